@@ -1,0 +1,265 @@
+"""ctypes wrapper of the fp64 C oracle (oracle/wasabi_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  The product path (paper_1708_04233_b200) never
+imports this module and shares no code with it.  Argument marshalling only: every step
+of the oracle's arithmetic is in the C file, which cites the paper passage it follows.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "wasabi_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain C, fp64, no FMA contraction, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fPIC",
+                               "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Params(C.Structure):
+    _fields_ = [("wavelength", C.c_double), ("pitch", C.c_double), ("n_h", C.c_int64),
+                ("n_depth", C.c_int32), ("levels", C.c_int32), ("z_min", C.c_double),
+                ("z_max", C.c_double), ("retention", C.c_double)]
+
+
+@dataclasses.dataclass(frozen=True)
+class Params:
+    wavelength: float
+    pitch: float
+    n_h: int
+    n_depth: int
+    levels: int
+    z_min: float
+    z_max: float
+    retention: float
+
+    @staticmethod
+    def from_config(cfg) -> "Params":
+        return Params(cfg.wavelength, cfg.pitch, cfg.n_h, cfg.n_depth, cfg.levels, cfg.z_min,
+                      cfg.z_max, cfg.retention)
+
+    def c(self) -> _Params:
+        return _Params(self.wavelength, self.pitch, self.n_h, self.n_depth, self.levels, self.z_min,
+                       self.z_max, self.retention)
+
+
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+_i8p = C.POINTER(C.c_int8)
+_u8p = C.POINTER(C.c_uint8)
+_pp = C.POINTER(_Params)
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = C.CDLL(build())
+            L.orc_geometry.argtypes = [_pp, _dp, _dp, _i64p, _i64p, _i64p, _i64p]
+            L.orc_depth_info.argtypes = [_pp, C.c_int, _dp, _i64p]
+            L.orc_psf_table.argtypes = [_pp, C.c_int, _dp]
+            L.orc_haar_fwd.argtypes = [_dp, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+            L.orc_haar_inv.argtypes = [_dp, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+            L.orc_table_coeffs.argtypes = [_pp, C.c_int, _dp]
+            L.orc_select.argtypes = [_pp, C.c_int, _i32p, _i32p, _i32p, _dp, C.c_int64]
+            L.orc_select.restype = C.c_int64
+            L.orc_lut_new.argtypes = [_pp]
+            L.orc_lut_new.restype = C.c_void_p
+            L.orc_lut_free.argtypes = [C.c_void_p]
+            L.orc_lut_build_depth.argtypes = [C.c_void_p, C.c_int]
+            L.orc_lut_build_depth.restype = C.c_int64
+            L.orc_points.argtypes = [_pp, _dp, C.c_int64, _i64p, _i64p, _i32p, _i8p]
+            L.orc_bins.argtypes = [_pp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, _i64p, _i32p,
+                                   C.c_int64]
+            L.orc_bins.restype = C.c_int64
+            L.orc_bin_tile.argtypes = [_pp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, _i32p,
+                                       C.c_int64]
+            L.orc_bin_tile.restype = C.c_int64
+            L.orc_wasabi_window.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                            C.c_int64, _dp]
+            L.orc_wasabi_window.restype = C.c_int64
+            L.orc_quantize.argtypes = [_pp, C.c_double, C.c_double, C.c_double, _dp, C.c_int64,
+                                       C.c_int64, C.c_int64, C.c_int64, _u8p, _dp]
+            L.orc_direct_d1.argtypes = [_pp, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                        _dp]
+            L.orc_direct_d2.argtypes = L.orc_direct_d1.argtypes
+            _lib = L
+    return _lib
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _pts64(pts) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(pts, dtype=np.float64).reshape(-1, 4))
+    return a
+
+
+def _cplx_buf(z: np.ndarray) -> np.ndarray:
+    """complex128 (h, w) -> contiguous float64 (h, w, 2) view copy."""
+    return np.ascontiguousarray(z.astype(np.complex128)).view(np.float64).reshape(z.shape + (2,))
+
+
+def geometry(P: Params) -> dict:
+    n = P.n_depth
+    z = np.zeros(n); R = np.zeros(n)
+    H = np.zeros(n, np.int64); E = np.zeros(n, np.int64)
+    nnz = np.zeros(n, np.int64); nr = np.zeros(n, np.int64)
+    lib().orc_geometry(C.byref(P.c()), _ptr(z, _dp), _ptr(R, _dp), _ptr(H, _i64p), _ptr(E, _i64p),
+                       _ptr(nnz, _i64p), _ptr(nr, _i64p))
+    return dict(z=z, R=R, H=H, E=E, nnz=nnz, n_r=nr)
+
+
+def psf_table(P: Params, d: int) -> np.ndarray:
+    H = int(geometry_one(P, d)["H"])
+    f = np.zeros((2 * H, 2 * H, 2))
+    lib().orc_psf_table(C.byref(P.c()), d, _ptr(f, _dp))
+    return f[..., 0] + 1j * f[..., 1]
+
+
+def geometry_one(P: Params, d: int) -> dict:
+    zr = np.zeros(2)
+    hen = np.zeros(4, np.int64)
+    lib().orc_depth_info(C.byref(P.c()), d, _ptr(zr, _dp), _ptr(hen, _i64p))
+    return dict(z=zr[0], R=zr[1], H=int(hen[0]), E=int(hen[1]), nnz=int(hen[2]), n_r=int(hen[3]))
+
+
+def haar_fwd(f: np.ndarray, L: int) -> np.ndarray:
+    b = _cplx_buf(f)
+    h, w = f.shape
+    lib().orc_haar_fwd(_ptr(b, _dp), h, w, w, L)
+    return b[..., 0] + 1j * b[..., 1]
+
+
+def haar_inv(f: np.ndarray, L: int) -> np.ndarray:
+    b = _cplx_buf(f)
+    h, w = f.shape
+    lib().orc_haar_inv(_ptr(b, _dp), h, w, w, L)
+    return b[..., 0] + 1j * b[..., 1]
+
+
+def table_coeffs(P: Params, d: int, H: int) -> np.ndarray:
+    c = np.zeros((2 * H, 2 * H, 2))
+    lib().orc_table_coeffs(C.byref(P.c()), d, _ptr(c, _dp))
+    return c[..., 0] + 1j * c[..., 1]
+
+
+def select(P: Params, d: int, cap: int):
+    lv = np.zeros(cap, np.int32); dx = np.zeros(cap, np.int32); dy = np.zeros(cap, np.int32)
+    val = np.zeros((cap, 2))
+    n = lib().orc_select(C.byref(P.c()), d, _ptr(lv, _i32p), _ptr(dx, _i32p), _ptr(dy, _i32p),
+                         _ptr(val, _dp), cap)
+    if n < 0:
+        raise ValueError("cap too small")
+    return lv[:n], dx[:n], dy[:n], val[:n, 0] + 1j * val[:n, 1]
+
+
+def points(P: Params, pts):
+    p = _pts64(pts)
+    n = p.shape[0]
+    ix = np.zeros(n, np.int64); iy = np.zeros(n, np.int64); iz = np.zeros(n, np.int32)
+    ok = np.zeros(n, np.int8)
+    lib().orc_points(C.byref(P.c()), _ptr(p, _dp), n, _ptr(ix, _i64p), _ptr(iy, _i64p), _ptr(iz, _i32p),
+                     _ptr(ok, _i8p))
+    return ix, iy, iz, ok.astype(bool)
+
+
+def bins(P: Params, T: int, pts, row0: int, row1: int, cap: int = None):
+    p = _pts64(pts)
+    n = p.shape[0]
+    nt = (P.n_h // T) * ((row1 - row0) // T)
+    ptr = np.zeros(nt + 1, np.int64)
+    cap = cap if cap is not None else max(1, n * 16)
+    while True:
+        idx = np.zeros(cap, np.int32)
+        tot = lib().orc_bins(C.byref(P.c()), T, _ptr(p, _dp), n, row0, row1, _ptr(ptr, _i64p),
+                             _ptr(idx, _i32p), cap)
+        if tot >= 0:
+            return ptr, idx[:tot]
+        cap = -tot
+
+
+def bin_tile(P: Params, T: int, pts, X0: int, Y0: int) -> np.ndarray:
+    p = _pts64(pts)
+    n = p.shape[0]
+    cap = max(1, n)
+    idx = np.zeros(cap, np.int32)
+    tot = lib().orc_bin_tile(C.byref(P.c()), T, _ptr(p, _dp), n, X0, Y0, _ptr(idx, _i32p), cap)
+    return idx[:tot]
+
+
+class Lut:
+    """Lazily built per-depth lists (orc_select) kept for repeated windows."""
+
+    def __init__(self, P: Params):
+        self.P = P
+        self._c = P.c()
+        self.h = lib().orc_lut_new(C.byref(self._c))
+
+    def build_depth(self, d: int) -> int:
+        return lib().orc_lut_build_depth(self.h, d)
+
+    def wasabi_window(self, pts, x0: int, y0: int, w: int, h: int):
+        """psi on hologram window [x0, x0+w) x [y0, y0+h) (Eq.(2)); returns (psi complex128, count)."""
+        p = _pts64(pts)
+        psi = np.zeros((h, w, 2))
+        cnt = lib().orc_wasabi_window(self.h, _ptr(p, _dp), p.shape[0], x0, y0, w, h, _ptr(psi, _dp))
+        return psi[..., 0] + 1j * psi[..., 1], cnt
+
+    def hologram_window(self, pts, x0: int, y0: int, w: int, h: int):
+        """u = inverse FWT of psi on a 2^L-aligned window (steps 2-3)."""
+        psi, cnt = self.wasabi_window(pts, x0, y0, w, h)
+        return haar_inv(psi, self.P.levels), psi, cnt
+
+    def close(self):
+        if self.h:
+            lib().orc_lut_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def quantize(P: Params, ref, u: np.ndarray, x0: int, y0: int):
+    h, w = u.shape
+    b = _cplx_buf(u)
+    bits = np.zeros((h, w // 8), np.uint8)
+    I = np.zeros((h, w))
+    lib().orc_quantize(C.byref(P.c()), float(ref[0]), float(ref[1]), float(ref[2]), _ptr(b, _dp), x0, y0,
+                       w, h, _ptr(bits, _u8p), _ptr(I, _dp))
+    return bits, I
+
+
+def direct_d1(P: Params, pts, x0: int, y0: int, w: int, h: int) -> np.ndarray:
+    p = _pts64(pts)
+    u = np.zeros((h, w, 2))
+    lib().orc_direct_d1(C.byref(P.c()), _ptr(p, _dp), p.shape[0], x0, y0, w, h, _ptr(u, _dp))
+    return u[..., 0] + 1j * u[..., 1]
+
+
+def direct_d2(P: Params, pts, x0: int, y0: int, w: int, h: int) -> np.ndarray:
+    p = _pts64(pts)
+    u = np.zeros((h, w, 2))
+    lib().orc_direct_d2(C.byref(P.c()), _ptr(p, _dp), p.shape[0], x0, y0, w, h, _ptr(u, _dp))
+    return u[..., 0] + 1j * u[..., 1]

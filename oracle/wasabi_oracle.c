@@ -1,0 +1,560 @@
+/*
+ * wasabi_oracle.c -- plain, slow, fp64 CPU oracle for the WASABI hot path of
+ * arXiv 1708.04233 ("Fast, large-scale hologram calculation in wavelet domain").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant with the CUDA path (paper_1708_04233_b200/csrc).
+ * Build: gcc -O2 -ffp-contract=off -fPIC -shared (no fast-math, no FMA contraction).
+ *
+ * Every function follows the paper (PAPER.md line numbers, section, equation)
+ * in the paper's order, with the readings listed in DESIGN.md §2 ("R-xx") where
+ * the paper is silent, ambiguous or garbled:
+ *   R-A1  Haar (orthonormal, 1/2 per 2-D level) instead of coiflets (north_star)
+ *   R-A2  PSF window radius rho_max = |z| tan(asin(lambda/2p)), S = {dx^2+dy^2 < R^2} U {(0,0)}
+ *   R-A3  depth levels z_d = z_min + d (z_max-z_min)/(N_z-1), nearest, ties to lower
+ *   R-A4  N_r,d = min(nnz_d, ceil(r_ppm nnz_d / 1e6)), nnz_d structural
+ *   R-A5  one joint ranking over all levels and subbands incl. LL, by |c|
+ *   R-A6  interleaved in-place Haar layout (Fig. 2(a) missing)
+ *   R-A8  per-level shift s_l = 2^l floor((ix + 2^(l-1)) / 2^l) ("alpha")
+ *   R-A9  ix = floor(x/p + 1/2) + N_h/2 (hologram-centred origin)
+ *   R-A11 bins in ascending point order; accumulation point-major, entry canonical order
+ *   R-A12 coefficients outside the hologram / band / window are dropped
+ *   R-A13 rank key kappa = fp32_RN(re^2+im^2), ties to the smaller linear index
+ *   R-A14 bit = Re(u conj(R)) >= 0
+ *   R-A15 R = exp(+i k sqrt((x-xr)^2+(y-yr)^2+zr^2))
+ *   R-A17 a <= 0, non-finite, or z beyond half a level outside the range: skipped
+ *
+ * Parity pins (tests/test_oracle_*.py) pin every function here to closed forms,
+ * invariants, brute force, or the paper's printed parameters; see DESIGN.md §4.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_PI 3.14159265358979323846
+
+typedef struct {
+    double wavelength;   /* lambda [m] (Eq.(1)) */
+    double pitch;        /* p [m], hologram sampling pitch */
+    int64_t n_h;         /* N_h, hologram side in pixels */
+    int32_t n_depth;     /* N_z */
+    int32_t levels;      /* L, wavelet levels (Haar here) */
+    double z_min, z_max; /* depth range [m] */
+    double retention;    /* r in (0,1] (north_star "top-r%") */
+} orc_params;
+
+/* ---------------------------------------------------------------- geometry */
+
+/* PAPER.md:90 PSF radius.  R-A2: maximum diffraction angle sin(theta) = lambda/(2p). */
+static double orc_tan_theta(const orc_params *P) {
+    double sigma = P->wavelength / (2.0 * P->pitch);
+    return sigma / sqrt(1.0 - sigma * sigma);
+}
+
+/* PAPER.md:91 depth discretisation; R-A3: inclusive endpoints. */
+static double orc_level_z(const orc_params *P, int d) {
+    if (P->n_depth <= 1) return P->z_min;
+    double dz = (P->z_max - P->z_min) / (double)(P->n_depth - 1);
+    return P->z_min + (double)d * dz;
+}
+
+/* R_d in pixels (R-A2). */
+static double orc_radius_px(const orc_params *P, double z) {
+    return fabs(z) * orc_tan_theta(P) / P->pitch;
+}
+
+/* Table half side H_d = 2^L (floor(R/2^L) + 1): table side 2H holds the disc and is 2^L aligned. */
+static int64_t orc_half(const orc_params *P, double R) {
+    int64_t B = (int64_t)1 << P->levels;
+    return B * ((int64_t)floor(R / (double)B) + 1);
+}
+
+/* S_d membership: circ(c) = 1 iff c < 1, centre always kept (R-A17). */
+static int orc_in_support(int64_t dx, int64_t dy, double R) {
+    if (dx == 0 && dy == 0) return 1;
+    return (double)(dx * dx + dy * dy) < R * R;
+}
+
+/* Structural nnz_d (R-A4): number of coefficient positions whose support block touches S_d.
+ * Brute force over the mask: level-l detail coefficients (3 per 2^l block) and level-L
+ * scaling coefficients (1 per 2^L block). */
+static int64_t orc_nnz(const orc_params *P, int64_t H, double R) {
+    int64_t side = 2 * H, nnz = 0;
+    unsigned char *m = (unsigned char *)calloc((size_t)(side * side), 1);
+    for (int64_t Y = 0; Y < side; Y++)
+        for (int64_t X = 0; X < side; X++) m[Y * side + X] = (unsigned char)orc_in_support(X - H, Y - H, R);
+    for (int l = 1; l <= P->levels; l++) {
+        int64_t b = (int64_t)1 << l;
+        for (int64_t Y0 = 0; Y0 < side; Y0 += b)
+            for (int64_t X0 = 0; X0 < side; X0 += b) {
+                int touch = 0;
+                for (int64_t y = Y0; y < Y0 + b && !touch; y++)
+                    for (int64_t x = X0; x < X0 + b; x++)
+                        if (m[y * side + x]) { touch = 1; break; }
+                if (touch) nnz += (l == P->levels) ? 4 : 3;
+            }
+    }
+    free(m);
+    return nnz;
+}
+
+/* R-A4: N_r,d = min(nnz, ceil(r_ppm * nnz / 1e6)), r_ppm = llround(r * 1e6). */
+static int64_t orc_n_r(const orc_params *P, int64_t nnz) {
+    int64_t r_ppm = llround(P->retention * 1e6);
+    int64_t n = (r_ppm * nnz + 999999) / 1000000;
+    return n < nnz ? n : nnz;
+}
+
+/* Per-depth geometry.  E_d = ceil(R_d) + 3*2^(L-1) is the footprint half-size (bins). */
+int orc_geometry(const orc_params *P, double *z, double *R, int64_t *H, int64_t *E, int64_t *nnz,
+                 int64_t *n_r) {
+    for (int d = 0; d < P->n_depth; d++) {
+        double zd = orc_level_z(P, d);
+        double Rd = orc_radius_px(P, zd);
+        int64_t Hd = orc_half(P, Rd);
+        if (z) z[d] = zd;
+        if (R) R[d] = Rd;
+        if (H) H[d] = Hd;
+        if (E) E[d] = (int64_t)ceil(Rd) + 3 * ((int64_t)1 << (P->levels - 1));
+        if (nnz || n_r) {
+            int64_t c = orc_nnz(P, Hd, Rd);
+            if (nnz) nnz[d] = c;
+            if (n_r) n_r[d] = orc_n_r(P, c);
+        }
+    }
+    return 0;
+}
+
+/* Geometry of one depth: zr = {z_d, R_d}, hen = {H_d, E_d, nnz_d, N_r,d}. */
+int orc_depth_info(const orc_params *P, int d, double *zr, int64_t *hen) {
+    double zd = orc_level_z(P, d), Rd = orc_radius_px(P, zd);
+    int64_t Hd = orc_half(P, Rd), c = orc_nnz(P, Hd, Rd);
+    zr[0] = zd; zr[1] = Rd;
+    hen[0] = Hd; hen[1] = (int64_t)ceil(Rd) + 3 * ((int64_t)1 << (P->levels - 1));
+    hen[2] = c; hen[3] = orc_n_r(P, c);
+    return 0;
+}
+
+/* ---------------------------------------------------------------- PSF (step 1) */
+
+/* u_z = exp(i k r) circ(.), unit amplitude (Eq.(1) carries only a_j).
+ * Table of side 2H, centre at (H, H); f is interleaved (re, im) row-major. */
+int orc_psf_table(const orc_params *P, int d, double *f) {
+    double z = orc_level_z(P, d), R = orc_radius_px(P, z);
+    int64_t H = orc_half(P, R), side = 2 * H;
+    double k = 2.0 * ORC_PI / P->wavelength;
+    for (int64_t Y = 0; Y < side; Y++)
+        for (int64_t X = 0; X < side; X++) {
+            int64_t dx = X - H, dy = Y - H;
+            double *o = f + 2 * (Y * side + X);
+            if (!orc_in_support(dx, dy, R)) { o[0] = 0.0; o[1] = 0.0; continue; }
+            double xp = (double)dx * P->pitch, yp = (double)dy * P->pitch;
+            double r = sqrt((xp * xp + yp * yp) + z * z);   /* r_hj */
+            double ph = k * r;
+            o[0] = cos(ph);
+            o[1] = sin(ph);
+        }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- Haar (steps 1, 3) */
+
+/* Forward FWT, R-A1/R-A6: level l = 1..L on every 2^l-aligned block, in place:
+ *   LL=((a+b)+(c+d))/2 at (X0,Y0), HL=((a-b)+(c-d))/2 at (X0+s,Y0),
+ *   LH=((a+b)-(c+d))/2 at (X0,Y0+s), HH=((a-b)-(c-d))/2 at (X0+s,Y0+s), s = 2^(l-1).
+ * f interleaved complex, row-major with row stride `stride` complex elements. */
+void orc_haar_fwd(double *f, int64_t rows, int64_t cols, int64_t stride, int L) {
+    for (int l = 1; l <= L; l++) {
+        int64_t b = (int64_t)1 << l, s = b >> 1;
+        for (int64_t Y0 = 0; Y0 < rows; Y0 += b)
+            for (int64_t X0 = 0; X0 < cols; X0 += b)
+                for (int c = 0; c < 2; c++) {
+                    double *pa = f + 2 * (Y0 * stride + X0) + c;
+                    double *pb = f + 2 * (Y0 * stride + X0 + s) + c;
+                    double *pc = f + 2 * ((Y0 + s) * stride + X0) + c;
+                    double *pd = f + 2 * ((Y0 + s) * stride + X0 + s) + c;
+                    double a = *pa, bb = *pb, cc = *pc, dd = *pd;
+                    *pa = ((a + bb) + (cc + dd)) / 2.0;
+                    *pb = ((a - bb) + (cc - dd)) / 2.0;
+                    *pc = ((a + bb) - (cc + dd)) / 2.0;
+                    *pd = ((a - bb) - (cc - dd)) / 2.0;
+                }
+    }
+}
+
+/* Inverse FWT (PAPER.md:94 step 3, :123): l = L..1,
+ *   a=((LL+HL)+(LH+HH))/2, b=((LL-HL)+(LH-HH))/2, c=((LL+HL)-(LH+HH))/2, d=((LL-HL)-(LH-HH))/2. */
+void orc_haar_inv(double *f, int64_t rows, int64_t cols, int64_t stride, int L) {
+    for (int l = L; l >= 1; l--) {
+        int64_t b = (int64_t)1 << l, s = b >> 1;
+        for (int64_t Y0 = 0; Y0 < rows; Y0 += b)
+            for (int64_t X0 = 0; X0 < cols; X0 += b)
+                for (int c = 0; c < 2; c++) {
+                    double *pa = f + 2 * (Y0 * stride + X0) + c;
+                    double *pb = f + 2 * (Y0 * stride + X0 + s) + c;
+                    double *pc = f + 2 * ((Y0 + s) * stride + X0) + c;
+                    double *pd = f + 2 * ((Y0 + s) * stride + X0 + s) + c;
+                    double LL = *pa, HL = *pb, LH = *pc, HH = *pd;
+                    *pa = ((LL + HL) + (LH + HH)) / 2.0;
+                    *pb = ((LL - HL) + (LH - HH)) / 2.0;
+                    *pc = ((LL + HL) - (LH + HH)) / 2.0;
+                    *pd = ((LL - HL) - (LH - HH)) / 2.0;
+                }
+    }
+}
+
+/* Level of an interleaved position (R-A6): t = min(ctz X, ctz Y); t >= L -> LL (level L),
+ * else level t+1.  Subband code: 0 LL, 1 HL, 2 LH, 3 HH. */
+static void orc_classify(int64_t X, int64_t Y, int L, int *level, int *band) {
+    int t = 0;
+    while (t < L && ((X >> t) & 1) == 0 && ((Y >> t) & 1) == 0) t++;
+    if (t >= L) { *level = L; *band = 0; return; }
+    *level = t + 1;
+    *band = (int)(((X >> t) & 1) | (((Y >> t) & 1) << 1));
+}
+
+/* ---------------------------------------------------------------- selection (step 1) */
+
+typedef struct { float kappa; int64_t lin; } orc_key;
+
+static int orc_key_cmp(const void *a, const void *b) {
+    const orc_key *x = (const orc_key *)a, *y = (const orc_key *)b;
+    if (x->kappa > y->kappa) return -1;       /* larger magnitude first */
+    if (x->kappa < y->kappa) return 1;
+    return (x->lin < y->lin) ? -1 : (x->lin > y->lin);   /* R-A13 tie-break */
+}
+
+typedef struct { int level; int64_t X, Y; } orc_pos;
+static int orc_canon_cmp(const void *a, const void *b) {
+    const orc_pos *x = (const orc_pos *)a, *y = (const orc_pos *)b;
+    if (x->level != y->level) return x->level - y->level;
+    if (x->Y != y->Y) return (x->Y < y->Y) ? -1 : 1;
+    return (x->X < y->X) ? -1 : (x->X > y->X);
+}
+
+/* Full transformed table of depth d (for invariant tests).  coef: (2H)^2 interleaved complex. */
+int orc_table_coeffs(const orc_params *P, int d, double *coef) {
+    orc_psf_table(P, d, coef);
+    double R = orc_radius_px(P, orc_level_z(P, d));
+    int64_t side = 2 * orc_half(P, R);
+    orc_haar_fwd(coef, side, side, side, P->levels);
+    return 0;
+}
+
+/* PAPER.md:92 "select N_r strong coefficients among the wavelet-domain PSF and store them in
+ * the LUT".  Full sort of all (2H)^2 positions by (kappa desc, linear index asc) (R-A13, R-A5),
+ * first N_r kept, then re-sorted canonically by (level, Y, X).  Outputs level, dx = X - H,
+ * dy = Y - H, fp64 value (re, im).  Returns the count (N_r,d) or -1 if cap is too small. */
+int64_t orc_select(const orc_params *P, int d, int32_t *level, int32_t *dx, int32_t *dy, double *val,
+                   int64_t cap) {
+    double z = orc_level_z(P, d), R = orc_radius_px(P, z);
+    int64_t H = orc_half(P, R), side = 2 * H, n = side * side;
+    int64_t nr = orc_n_r(P, orc_nnz(P, H, R));
+    if (nr > cap) return -1;
+    double *c = (double *)malloc(sizeof(double) * 2 * (size_t)n);
+    orc_table_coeffs(P, d, c);
+    orc_key *keys = (orc_key *)malloc(sizeof(orc_key) * (size_t)n);
+    for (int64_t i = 0; i < n; i++) {
+        double re = c[2 * i], im = c[2 * i + 1];
+        double m2 = re * re + im * im;
+        keys[i].kappa = (float)m2;         /* fp32 round-to-nearest of the fp64 |c|^2 */
+        keys[i].lin = i;                   /* Y * side + X */
+    }
+    qsort(keys, (size_t)n, sizeof(orc_key), orc_key_cmp);
+    orc_pos *sel = (orc_pos *)malloc(sizeof(orc_pos) * (size_t)(nr > 0 ? nr : 1));
+    for (int64_t i = 0; i < nr; i++) {
+        int lv, bd;
+        sel[i].X = keys[i].lin % side;
+        sel[i].Y = keys[i].lin / side;
+        orc_classify(sel[i].X, sel[i].Y, P->levels, &lv, &bd);
+        sel[i].level = lv;
+    }
+    qsort(sel, (size_t)nr, sizeof(orc_pos), orc_canon_cmp);
+    for (int64_t i = 0; i < nr; i++) {
+        int64_t X = sel[i].X, Y = sel[i].Y;
+        level[i] = sel[i].level;
+        dx[i] = (int32_t)(X - H);
+        dy[i] = (int32_t)(Y - H);
+        val[2 * i] = c[2 * (Y * side + X)];
+        val[2 * i + 1] = c[2 * (Y * side + X) + 1];
+    }
+    free(sel);
+    free(keys);
+    free(c);
+    return nr;
+}
+
+/* ---------------------------------------------------------------- LUT cache */
+
+typedef struct {
+    int built;
+    int64_t n, H;
+    int32_t *level, *dx, *dy;
+    double *val;
+} orc_depth_list;
+
+typedef struct {
+    orc_params P;
+    orc_depth_list *lists;
+} orc_lut;
+
+void *orc_lut_new(const orc_params *P) {
+    orc_lut *t = (orc_lut *)calloc(1, sizeof(orc_lut));
+    t->P = *P;
+    t->lists = (orc_depth_list *)calloc((size_t)P->n_depth, sizeof(orc_depth_list));
+    return t;
+}
+
+void orc_lut_free(void *h) {
+    orc_lut *t = (orc_lut *)h;
+    if (!t) return;
+    for (int d = 0; d < t->P.n_depth; d++) {
+        free(t->lists[d].level); free(t->lists[d].dx); free(t->lists[d].dy); free(t->lists[d].val);
+    }
+    free(t->lists);
+    free(t);
+}
+
+static orc_depth_list *orc_lut_get(orc_lut *t, int d) {
+    orc_depth_list *L = &t->lists[d];
+    if (L->built) return L;
+    const orc_params *P = &t->P;
+    double R = orc_radius_px(P, orc_level_z(P, d));
+    L->H = orc_half(P, R);
+    int64_t cap = orc_n_r(P, orc_nnz(P, L->H, R));
+    L->level = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cap + 1));
+    L->dx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cap + 1));
+    L->dy = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cap + 1));
+    L->val = (double *)malloc(sizeof(double) * 2 * (size_t)(cap + 1));
+    L->n = orc_select(P, d, L->level, L->dx, L->dy, L->val, cap);
+    L->built = 1;
+    return L;
+}
+
+/* Build (force) the list of depth d in the cache; returns N_r,d. */
+int64_t orc_lut_build_depth(void *h, int d) { return orc_lut_get((orc_lut *)h, d)->n; }
+
+/* ---------------------------------------------------------------- points (step 2a) */
+
+/* R-A9 / R-A3 / R-A17: point -> (ix, iy, iz), valid flag.  pts is (n, 4) fp64 (x, y, z, a). */
+static int orc_point(const orc_params *P, const double *pt, int64_t *ix, int64_t *iy, int *iz) {
+    double x = pt[0], y = pt[1], z = pt[2], a = pt[3];
+    if (!isfinite(x) || !isfinite(y) || !isfinite(z) || !isfinite(a) || !(a > 0.0)) return 0;
+    double u = x / P->pitch, v = y / P->pitch;
+    if (!(fabs(u) <= 1073741824.0) || !(fabs(v) <= 1073741824.0)) return 0;
+    *ix = (int64_t)floor(u + 0.5) + P->n_h / 2;
+    *iy = (int64_t)floor(v + 0.5) + P->n_h / 2;
+    if (P->n_depth <= 1) { *iz = 0; return 1; }
+    double dz = (P->z_max - P->z_min) / (double)(P->n_depth - 1);
+    double t = (z - P->z_min) / dz;
+    if (t < -0.5 || t > (double)(P->n_depth - 1) + 0.5) return 0;
+    int64_t q = (int64_t)ceil(t - 0.5);          /* nearest level, ties to the lower index */
+    if (q < 0) q = 0;
+    if (q > P->n_depth - 1) q = P->n_depth - 1;
+    *iz = (int)q;
+    return 1;
+}
+
+int orc_points(const orc_params *P, const double *pts, int64_t n, int64_t *ix, int64_t *iy, int32_t *iz,
+               int8_t *valid) {
+    for (int64_t j = 0; j < n; j++) {
+        int64_t a = 0, b = 0;
+        int c = 0;
+        valid[j] = (int8_t)orc_point(P, pts + 4 * j, &a, &b, &c);
+        ix[j] = a; iy[j] = b; iz[j] = c;
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- bins (step 2a) */
+
+/* PAPER.md:115-122 sub-hologram re-basing, applied per T x T tile (R-A12): point j is in
+ * bin(tx,ty) iff its footprint box [ix-E, ix+E] x [iy-E, iy+E] meets the tile and the tile
+ * lies in rows [row0, row1).  Brute force over all tiles of the band, points ascending.
+ * tile_ptr has n_tiles+1 entries (tiles row-major within the band).  Returns total entries,
+ * or -(needed) if cap is too small (idx untouched beyond cap). */
+int64_t orc_bins(const orc_params *P, int64_t T, const double *pts, int64_t n, int64_t row0, int64_t row1,
+                 int64_t *tile_ptr, int32_t *idx, int64_t cap) {
+    int64_t tiles_x = P->n_h / T, tiles_y = (row1 - row0) / T;
+    double *Rz = (double *)malloc(sizeof(double) * (size_t)P->n_depth);
+    for (int d = 0; d < P->n_depth; d++) Rz[d] = orc_radius_px(P, orc_level_z(P, d));
+    int64_t half = (int64_t)1 << (P->levels - 1);
+    int64_t *bx = (int64_t *)malloc(sizeof(int64_t) * 4 * (size_t)(n > 0 ? n : 1));
+    int8_t *ok = (int8_t *)malloc((size_t)(n > 0 ? n : 1));
+    for (int64_t j = 0; j < n; j++) {
+        int64_t ix, iy;
+        int iz;
+        ok[j] = (int8_t)orc_point(P, pts + 4 * j, &ix, &iy, &iz);
+        if (!ok[j]) continue;
+        int64_t E = (int64_t)ceil(Rz[iz]) + 3 * half;
+        bx[4 * j + 0] = ix - E; bx[4 * j + 1] = ix + E;
+        bx[4 * j + 2] = iy - E; bx[4 * j + 3] = iy + E;
+    }
+    int64_t total = 0;
+    for (int64_t ty = 0; ty < tiles_y; ty++)
+        for (int64_t tx = 0; tx < tiles_x; tx++) {
+            int64_t t = ty * tiles_x + tx;
+            int64_t X0 = tx * T, X1 = X0 + T - 1, Y0 = row0 + ty * T, Y1 = Y0 + T - 1;
+            tile_ptr[t] = total;
+            for (int64_t j = 0; j < n; j++) {
+                if (!ok[j]) continue;
+                if (bx[4 * j + 1] < X0 || bx[4 * j + 0] > X1) continue;
+                if (bx[4 * j + 3] < Y0 || bx[4 * j + 2] > Y1) continue;
+                if (total < cap) idx[total] = (int32_t)j;
+                total++;
+            }
+        }
+    tile_ptr[tiles_x * tiles_y] = total;
+    free(ok); free(bx); free(Rz);
+    return total <= cap ? total : -total;
+}
+
+/* One bin by the same definition (for sampled parity at full size): points ascending whose box
+ * meets tile [X0, X0+T) x [Y0, Y0+T) (absolute hologram rows).  Returns the count. */
+int64_t orc_bin_tile(const orc_params *P, int64_t T, const double *pts, int64_t n, int64_t X0, int64_t Y0,
+                     int32_t *idx, int64_t cap) {
+    int64_t half = (int64_t)1 << (P->levels - 1), total = 0;
+    for (int64_t j = 0; j < n; j++) {
+        int64_t ix, iy;
+        int iz;
+        if (!orc_point(P, pts + 4 * j, &ix, &iy, &iz)) continue;
+        int64_t E = (int64_t)ceil(orc_radius_px(P, orc_level_z(P, iz))) + 3 * half;
+        if (ix + E < X0 || ix - E > X0 + T - 1 || iy + E < Y0 || iy - E > Y0 + T - 1) continue;
+        if (total < cap) idx[total] = (int32_t)j;
+        total++;
+    }
+    return total;
+}
+
+/* ---------------------------------------------------------------- WASABI (steps 2b, 3) */
+
+static int64_t orc_floor_div(int64_t a, int64_t b) {  /* b > 0 */
+    int64_t q = a / b;
+    if ((a % b != 0) && (a < 0)) q--;
+    return q;
+}
+
+/* Eq.(2), with the sub-hologram re-basing of PAPER.md:121-122 replaced by a
+ * window [x0, x0+w) x [y0, y0+h) of the full hologram (R-A12: coefficients outside the window or
+ * outside [0, N_h)^2 are dropped).  psi(m, n) = sum_j a_j sum_k c_{z_j,k} delta(...) with the
+ * level shift s_l = 2^l floor((ix + 2^(l-1)) / 2^l) (R-A8).  psi: h x w interleaved complex,
+ * overwritten.  Points ascending, list entries in canonical order (R-A11).
+ * Returns the number of in-window accumulations. */
+int64_t orc_wasabi_window(void *lut, const double *pts, int64_t n, int64_t x0, int64_t y0, int64_t w,
+                          int64_t h, double *psi) {
+    orc_lut *t = (orc_lut *)lut;
+    const orc_params *P = &t->P;
+    memset(psi, 0, sizeof(double) * 2 * (size_t)(w * h));
+    int64_t count = 0, half = (int64_t)1 << (P->levels - 1);
+    for (int64_t j = 0; j < n; j++) {
+        int64_t ix, iy;
+        int iz;
+        if (!orc_point(P, pts + 4 * j, &ix, &iy, &iz)) continue;
+        double R = orc_radius_px(P, orc_level_z(P, iz));
+        int64_t E = (int64_t)ceil(R) + 3 * half;
+        if (ix + E < x0 || ix - E >= x0 + w || iy + E < y0 || iy - E >= y0 + h) continue;
+        orc_depth_list *L = orc_lut_get(t, iz);
+        double a = pts[4 * j + 3];
+        for (int64_t k = 0; k < L->n; k++) {
+            int l = L->level[k];
+            int64_t b = (int64_t)1 << l, hb = b >> 1;
+            int64_t sx = b * orc_floor_div(ix + hb, b);
+            int64_t sy = b * orc_floor_div(iy + hb, b);
+            int64_t X = sx + L->dx[k], Y = sy + L->dy[k];
+            if (X < 0 || X >= P->n_h || Y < 0 || Y >= P->n_h) continue;
+            if (X < x0 || X >= x0 + w || Y < y0 || Y >= y0 + h) continue;
+            double *o = psi + 2 * ((Y - y0) * w + (X - x0));
+            o[0] += a * L->val[2 * k];
+            o[1] += a * L->val[2 * k + 1];
+            count++;
+        }
+    }
+    return count;
+}
+
+/* ---------------------------------------------------------------- quantise (step 4) */
+
+/* PAPER.md:135 (spherical reference at (x_r, y_r, z_r)) and :137 (binary amplitude), R-A14/A15.
+ * u: h x w interleaved complex for hologram pixels [x0, x0+w) x [y0, y0+h).
+ * bits: h x (w/8) bytes, pixel X -> byte (X - x0) >> 3, bit 7 - ((X - x0) & 7); 1 = I >= 0.
+ * I_out (optional): the interference term I = Re(u conj(R)). */
+int orc_quantize(const orc_params *P, double xr, double yr, double zr, const double *u, int64_t x0,
+                 int64_t y0, int64_t w, int64_t h, uint8_t *bits, double *I_out) {
+    double k = 2.0 * ORC_PI / P->wavelength;
+    memset(bits, 0, (size_t)(h * (w / 8)));
+    for (int64_t Y = y0; Y < y0 + h; Y++)
+        for (int64_t X = x0; X < x0 + w; X++) {
+            double x = (double)(X - P->n_h / 2) * P->pitch, y = (double)(Y - P->n_h / 2) * P->pitch;
+            double ddx = x - xr, ddy = y - yr;
+            double r = sqrt((ddx * ddx + ddy * ddy) + zr * zr);
+            double ph = k * r;
+            double Rr = cos(ph), Ri = sin(ph);
+            const double *uu = u + 2 * ((Y - y0) * w + (X - x0));
+            double I = uu[0] * Rr + uu[1] * Ri;     /* Re(u conj(R)) */
+            if (I_out) I_out[(Y - y0) * w + (X - x0)] = I;
+            if (I >= 0.0) bits[(Y - y0) * (w / 8) + ((X - x0) >> 3)] |= (uint8_t)(0x80u >> ((X - x0) & 7));
+        }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- direct sums (Eq.(1)) */
+
+/* D1: exact Eq.(1) on a window, continuous (x_j, y_j, z_j), with the
+ * diffraction-limited window rho < |z_j| tan(theta) (+ the rho = 0 pixel), evaluated in
+ * pixel units.  Per-pixel double loop (the O(N N_h^2) form of PAPER.md:76). */
+int orc_direct_d1(const orc_params *P, const double *pts, int64_t n, int64_t x0, int64_t y0, int64_t w,
+                  int64_t h, double *u) {
+    double k = 2.0 * ORC_PI / P->wavelength, tn = orc_tan_theta(P);
+    for (int64_t Y = y0; Y < y0 + h; Y++)
+        for (int64_t X = x0; X < x0 + w; X++) {
+            double sr = 0.0, si = 0.0;
+            double xh = (double)(X - P->n_h / 2) * P->pitch, yh = (double)(Y - P->n_h / 2) * P->pitch;
+            for (int64_t j = 0; j < n; j++) {
+                const double *q = pts + 4 * j;
+                if (!isfinite(q[0]) || !isfinite(q[1]) || !isfinite(q[2]) || !(q[3] > 0.0)) continue;
+                double ex = (double)(X - P->n_h / 2) - q[0] / P->pitch;
+                double ey = (double)(Y - P->n_h / 2) - q[1] / P->pitch;
+                double rho2 = ex * ex + ey * ey;
+                double Rj = fabs(q[2]) * tn / P->pitch;
+                if (!(rho2 < Rj * Rj) && rho2 != 0.0) continue;
+                double ddx = xh - q[0], ddy = yh - q[1];
+                double r = sqrt((ddx * ddx + ddy * ddy) + q[2] * q[2]);
+                sr += q[3] * cos(k * r);
+                si += q[3] * sin(k * r);
+            }
+            u[2 * ((Y - y0) * w + (X - x0))] = sr;
+            u[2 * ((Y - y0) * w + (X - x0)) + 1] = si;
+        }
+    return 0;
+}
+
+/* D2: quantised direct sum ("PSF stamping", the N-LUT-like form): snapped (ix, iy), level depth
+ * z_iz and integer support S_iz, summed point by point. */
+int orc_direct_d2(const orc_params *P, const double *pts, int64_t n, int64_t x0, int64_t y0, int64_t w,
+                  int64_t h, double *u) {
+    double k = 2.0 * ORC_PI / P->wavelength;
+    memset(u, 0, sizeof(double) * 2 * (size_t)(w * h));
+    for (int64_t j = 0; j < n; j++) {
+        int64_t ix, iy;
+        int iz;
+        if (!orc_point(P, pts + 4 * j, &ix, &iy, &iz)) continue;
+        double z = orc_level_z(P, iz), R = orc_radius_px(P, z);
+        int64_t Rc = (int64_t)ceil(R) + 1;
+        for (int64_t Y = iy - Rc; Y <= iy + Rc; Y++) {
+            if (Y < y0 || Y >= y0 + h) continue;
+            for (int64_t X = ix - Rc; X <= ix + Rc; X++) {
+                if (X < x0 || X >= x0 + w) continue;
+                int64_t dx = X - ix, dy = Y - iy;
+                if (!orc_in_support(dx, dy, R)) continue;
+                double xp = (double)dx * P->pitch, yp = (double)dy * P->pitch;
+                double r = sqrt((xp * xp + yp * yp) + z * z);
+                double *o = u + 2 * ((Y - y0) * w + (X - x0));
+                o[0] += pts[4 * j + 3] * cos(k * r);
+                o[1] += pts[4 * j + 3] * sin(k * r);
+            }
+        }
+    }
+    return 0;
+}
