@@ -1,0 +1,195 @@
+/*
+ * wasabi.h -- C ABI of the B200-native WASABI hot path (arXiv 1708.04233,
+ * "Fast, large-scale hologram calculation in wavelet domain"; PAPER.md in the
+ * reference).  Library: paper_1708_04233_b200/libwasabi.so (sm_100a kernels).
+ *
+ * The path (Sec. 1, :86-95 and :115-125):
+ *   step 1  wasabi_build_psf_tables  per-depth PSF u_z = exp(ikr) circ(.),
+ *           depth-discretised (:91), forward Haar FWT (:91, Haar per north_star instead of
+ *           the paper's coiflets :106), top-N_r strong coefficients kept in a LUT (:92).
+ *   step 2a wasabi_bin_points        object points (x, y, z, a) (Eq.(1), :70-75) converted to
+ *           pixels/levels and binned to the T x T tiles their PSF footprint overlaps -- the
+ *           paper's sub-hologram re-basing x'_j = x_j - s N_h (:115-122) applied per tile.
+ *   step 2b wasabi_superpose         Eq.(2) (:108-113): psi(m,n) = sum_j a_j sum_k c_{z_j,k}
+ *           delta(m - alpha x_j, n - alpha y_j), alpha = 2^-l per level (reading R-A8).
+ *   step 3  wasabi_inverse_wt        inverse FWT of psi (:94, :123), optionally fused with
+ *   step 4  wasabi_quantize          binary-amplitude print pattern against a spherical
+ *           reference wave (:135, :137).
+ * Readings of the paper where it is silent/garbled are listed in DESIGN.md §2 (R-xx).
+ *
+ * Conventions (all entry points):
+ *  - Ownership: the CALLER allocates and frees every device buffer.  The library never
+ *    allocates device memory (wasabi_hologram_host copies into a caller-provided workspace).
+ *  - Streams: every compute call is asynchronous on `stream` (cudaStream_t; NULL = legacy
+ *    default stream).  Size queries are host-only.  export/stats/check calls synchronise.
+ *  - Errors: functions return wasabi_status; on a non-OK status wasabi_last_error() returns a
+ *    thread-local message.  WASABI_EINVAL = parameter violation (message names it),
+ *    WASABI_ENOSPC = buffer too small (message gives the required bytes), WASABI_ECUDA = a CUDA
+ *    launch/API error, WASABI_ESTATE = a buffer built with other parameters.
+ *  - Point-level problems never fail a call (non-finite coordinates, a <= 0, z more than half
+ *    a level outside [z_min, z_max]): such points are skipped and counted (wasabi_bins_stats).
+ *  - Pixel convention: hologram pixel (X, Y) is at ((X - N_h/2) p, (Y - N_h/2) p) metres
+ *    (hologram-centred origin, reading R-A9).  Fields are row-major, Y slowest.
+ *  - Complex fields are interleaved float32 (re, im) = "complex64", 8 bytes per pixel.
+ *  - Bands: [row0, row1) is a band of hologram rows; row0 and row1 must be multiples of
+ *    params.tile.  All band buffers hold only the band: (row1-row0) x N_h pixels.
+ */
+#ifndef WASABI_H
+#define WASABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    WASABI_OK = 0,
+    WASABI_EINVAL = -1,
+    WASABI_ENOSPC = -2,
+    WASABI_ECUDA = -3,
+    WASABI_ESTATE = -4
+} wasabi_status;
+
+/* Problem parameters -- the paper's problem statement (Eq.(1) inputs; depth
+ * discretisation :91; wavelet levels :106) plus the GPU tile side. */
+typedef struct {
+    double wavelength_m;  /* lambda > 0; Nyquist: lambda < 2 * pitch, else EINVAL   */
+    double pitch_m;       /* pixel pitch p > 0                                      */
+    int64_t n_h;          /* square hologram side N_h; multiple of tile                            */
+    int32_t n_depth;      /* N_z >= 1 depth levels                              */
+    int32_t levels;       /* Haar levels L, 1..6                                                    */
+    double z_min_m;       /* level centres z_d = z_min + d (z_max - z_min)/(N_z - 1) (R-A3)         */
+    double z_max_m;       /* z_max >= z_min; N_z = 1 uses z_min only                                */
+    double retention;     /* r in (0, 1]: N_r,d = min(nnz_d, ceil(r_ppm nnz_d / 1e6)), r_ppm =
+                             llround(r 1e6) >= 1 (R-A4; the paper's N_r = pi (W/2)^2 gamma, :92)   */
+    int32_t tile;         /* T: bin / superposition tile side; 64 or 128 (multiple of 2^L)        */
+    uint32_t flags;       /* reserved, must be 0                                                    */
+} wasabi_params;
+
+/* Spherical reference wave point (paper default (0, 0.030, -0.400) m). */
+typedef struct {
+    double x_r_m, y_r_m, z_r_m;
+} wasabi_print_params;
+
+/* Host-side geometry of one depth level (no device access). */
+typedef struct {
+    double z_m;           /* level depth z_d                                                       */
+    double radius_px;     /* R_d = |z_d| tan(asin(lambda/2p)) / p (reading R-A2)      */
+    int64_t half;         /* H_d: PSF table side is 2 H_d, centre at (H_d, H_d)                    */
+    int64_t footprint;    /* E_d = ceil(R_d) + 3 2^(L-1): footprint half-size used for binning     */
+    int64_t nnz;          /* structural nonzero wavelet coefficients (blocks touching the disc)   */
+    int64_t n_r;          /* N_r,d kept coefficients                                               */
+} wasabi_depth_info;
+
+/* ---------------------------------------------------------------- step 1 */
+
+/* Bytes of the table buffer (device, immutable after build) and of the build scratch. */
+wasabi_status wasabi_psf_tables_bytes(const wasabi_params *params, size_t *table_bytes,
+                                      size_t *scratch_bytes);
+
+/* Step 1: for every depth level, PSF -> L-level forward Haar (fp64) -> keep the
+ * N_r,d coefficients with the largest fp32(|c|^2), ties to the smaller table index (R-A13) ->
+ * LUT.  d_tables (table_bytes) and d_scratch (scratch_bytes) are caller-owned device buffers;
+ * d_tables is fully (re)written and self-describing; d_scratch may be reused after the stream
+ * passes this call.  Alignment: 256 bytes. */
+wasabi_status wasabi_build_psf_tables(const wasabi_params *params, void *d_tables, size_t table_bytes,
+                                      void *d_scratch, size_t scratch_bytes, cudaStream_t stream);
+
+/* Geometry of depth `depth` (host only). */
+wasabi_status wasabi_depth_geometry(const wasabi_params *params, int32_t depth, wasabi_depth_info *out);
+
+/* ---------------------------------------------------------------- step 2a */
+
+/* Upper bound of the bin buffer for n points and band [row0, row1) (host only, no sync). */
+wasabi_status wasabi_bin_points_bytes(const wasabi_params *params, int64_t n, int64_t row0, int64_t row1,
+                                      size_t *bin_bytes);
+
+/* Step 2a: convert points to (ix, iy, iz) in fp64 (R-A3, R-A9, R-A17) and
+ * build, for every T x T tile of band [row0, row1), the list of points (ascending index,
+ * R-A11) whose footprint box [ix +- E] x [iy +- E] meets the tile.
+ * d_points: n x 4 float32 (x, y, z, a) [m, m, m, -], 16-byte aligned, n >= 0.
+ * d_bins: bin_bytes from wasabi_bin_points_bytes (or more); fully rewritten.
+ * d_tables: built by wasabi_build_psf_tables with the same params. */
+wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_tables, const float *d_points,
+                                int64_t n, int64_t row0, int64_t row1, void *d_bins, size_t bin_bytes,
+                                cudaStream_t stream);
+
+/* ---------------------------------------------------------------- step 2b */
+
+/* Step 2b, Eq.(2): psi for band [row0, row1) (must equal the bins' band) in
+ * the interleaved in-place Haar layout (R-A6).  Coefficient (l, dX, dY, c) of point j lands at
+ * X = s_l(ix_j) + dX, Y = s_l(iy_j) + dY with s_l(i) = 2^l floor((i + 2^(l-1)) / 2^l) (R-A8);
+ * contributions outside the hologram or band are dropped (R-A12).  One CTA owns each tile in
+ * shared memory, no global atomics; per-pixel accumulation order is fixed (deterministic).
+ * d_psi: (row1 - row0) x n_h complex64, overwritten. */
+wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables, const void *d_bins,
+                               int64_t row0, int64_t row1, float *d_psi, cudaStream_t stream);
+
+/* ---------------------------------------------------------------- steps 3 (+4) */
+
+/* Step 3: L-level inverse Haar, tile-local (band rows multiples of 2^L, so
+ * no halo).  d_u may alias d_psi (in place).  d_u == NULL: u is not written (print only).
+ * d_bits != NULL fuses step 4 (see wasabi_quantize) and requires `print`. */
+wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi, float *d_u, int64_t row0,
+                                int64_t row1, const wasabi_print_params *print, uint8_t *d_bits,
+                                cudaStream_t stream);
+
+/* Step 4: R = exp(+i k sqrt((x-x_r)^2 + (y-y_r)^2 + z_r^2)) with the phase
+ * reduced in fp64 (R-A15), I = Re(u conj(R)), bit = (I >= 0) (R-A14).  d_bits: (row1-row0) x
+ * n_h/8 bytes, pixel X -> byte X >> 3, bit 7 - (X & 7) (MSB first); 1 = transparent. */
+wasabi_status wasabi_quantize(const wasabi_params *params, const wasabi_print_params *print, const float *d_u,
+                              int64_t row0, int64_t row1, uint8_t *d_bits, cudaStream_t stream);
+
+/* ---------------------------------------------------------------- whole path, host buffers */
+
+/* Device workspace for wasabi_hologram_host (tables + scratch + points + bins + field). */
+wasabi_status wasabi_hologram_workspace_bytes(const wasabi_params *params, int64_t n, int64_t row0,
+                                              int64_t row1, size_t *workspace_bytes);
+
+/* Whole hot path from HOST buffers: H2D copy of h_points (n x 4 float32), steps 1-4 for band
+ * [row0, row1), D2H copy of the bits (h_bits, (row1-row0) x n_h/8 bytes) and, if h_u != NULL,
+ * of u ((row1-row0) x n_h complex64).  Host buffers should be pinned for asynchronous copies.
+ * Returns after enqueueing; the caller synchronises `stream` before reading h_bits / h_u. */
+wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_print_params *print,
+                                   const float *h_points, int64_t n, int64_t row0, int64_t row1,
+                                   void *d_workspace, size_t workspace_bytes, uint8_t *h_bits, float *h_u,
+                                   cudaStream_t stream);
+
+/* ---------------------------------------------------------------- diagnostics (synchronous) */
+
+/* Verify that d_tables was built with these params (header magic + parameter hash). */
+wasabi_status wasabi_tables_check(const wasabi_params *params, const void *d_tables);
+
+/* Export the kept coefficients of one depth in canonical (level, Y, X) order (R-A5): level l
+ * (LL counts as level L), dX = X - H_d, dY = Y - H_d, value (re, im) float32.  Host arrays of
+ * capacity cap; *n_out = N_r,d (ENOSPC if cap is smaller). */
+wasabi_status wasabi_export_table(const wasabi_params *params, const void *d_tables, int32_t depth,
+                                  int32_t *h_level, int32_t *h_dx, int32_t *h_dy, float *h_val, int64_t cap,
+                                  int64_t *n_out);
+
+/* Export bins: h_tile_ptr (n_tiles + 1, tiles row-major within the band) and h_point_idx
+ * (cap entries); *n_out = total entries (ENOSPC if cap is smaller). */
+wasabi_status wasabi_export_bins(const wasabi_params *params, const void *d_bins, int64_t *h_tile_ptr,
+                                 int32_t *h_point_idx, int64_t cap, int64_t *n_out);
+
+/* Bin statistics: out[0] valid points, out[1] skipped points, out[2] bin entries, out[3] bin
+ * capacity, out[4] row0, out[5] row1, out[6] number of tiles, out[7] status (0 = ok). */
+wasabi_status wasabi_bins_stats(const void *d_bins, int64_t out[8]);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char *wasabi_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process (diagnostic counter). */
+unsigned long long wasabi_kernel_launches(void);
+
+/* Library version string. */
+const char *wasabi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WASABI_H */

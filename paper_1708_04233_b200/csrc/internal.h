@@ -1,0 +1,98 @@
+// internal.h -- device buffer layouts and kernel launchers of libwasabi (product side only).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wasabi {
+
+constexpr uint64_t kTableMagic = 0x3142545942415357ull;  // "WSABYTB1"
+constexpr uint64_t kBinMagic = 0x314e494249425357ull;    // "WSBIBIN1"
+constexpr int kMaxLevels = 6;
+constexpr int kMaxTableSide = 16384;  // 2H limit: packed positions use 13/14-bit block indices
+
+// Compact per-depth data read by the hot kernels (32 bytes).
+struct KDesc {
+    int32_t H;                    // table half side
+    int32_t E;                    // footprint half-size (binning)
+    int32_t ptr_base[kMaxLevels]; // level l (1..L) band pointer rows start at ptr_base[l-1]
+};
+
+// Per-depth data used by the table build and exports.
+struct DDesc {
+    double z, R;
+    int64_t nnz, n_r;
+    int64_t coef_off;   // element offset of this depth's (2H)^2 table in the build scratch
+    int32_t side;       // 2H
+    int32_t tiles;      // ceil(side / 64) tiles per side for K1
+    int32_t cta_base;   // prefix of K1 CTAs (tiles^2)
+    int32_t group_base; // prefix of (level, band, Xb) groups (== its ptr_base for level 1)
+    int32_t n_groups;
+    int32_t pad;
+};
+
+struct TableHeader {
+    uint64_t magic;
+    uint64_t param_hash;
+    int32_t n_depth, levels, tile, S;  // S = smem row stride baked into packed positions
+    int64_t total_entries;             // sum N_r,d
+    int64_t total_ptrs;                // int32 pointer slots
+    int64_t total_ctas;                // K1 grid
+    int64_t kdesc_off, ddesc_off, val_off, pos_off, ptr_off, ctabase_off;  // byte offsets
+    int64_t table_bytes;
+    int64_t pad[3];
+};
+
+struct BinHeader {
+    uint64_t magic;
+    uint64_t param_hash;
+    int64_t n_points, row0, row1;
+    int32_t T, tiles_x, tiles_y, pad0;
+    int64_t n_tiles, capacity;
+    int64_t pts_off, ptr_off, cnt_off, idx_off, idx2_off, scan_off;  // byte offsets
+    int64_t bin_bytes;
+    // device-written statistics
+    unsigned long long n_valid, n_skipped, total_entries, status;
+    int64_t pad[2];
+};
+
+// Band height (pixels) of the per-level pointer index: T/4, >= 2^l (hb_l = max(1, (T/4) >> l)).
+__host__ __device__ inline int band_blocks(int T, int l) {
+    int hb = (T / 4) >> l;
+    return hb < 1 ? 1 : hb;
+}
+
+// ---- table geometry computed on host (L0) ----
+struct LevelGeom {
+    int nb, hb, nbands;   // blocks per row, band height (blocks), bands
+};
+
+// Number of kernels this library has launched (process-wide, relaxed atomic).
+void count_launches(int n);
+
+// ---- launchers ----
+cudaError_t launch_psf_haar(const TableHeader &h, const void *d_tables, float2 *coef_val, uint32_t *coef_key,
+                            double k, double pitch, int levels, int n_depth, cudaStream_t s);
+cudaError_t launch_select(const TableHeader &h, const void *d_tables, const uint32_t *coef_key,
+                          unsigned int *hist, unsigned long long *sel_state, int n_depth, cudaStream_t s);
+cudaError_t launch_groups(const TableHeader &h, void *d_tables, const float2 *coef_val, const uint32_t *coef_key,
+                          const unsigned long long *sel_state, int pass, cudaStream_t s);
+cudaError_t launch_scan_i32(int32_t *data, int64_t n, void *scratch, cudaStream_t s);
+cudaError_t launch_scan_u32_to_u64(const uint32_t *in, unsigned long long *out, int64_t n, void *scratch,
+                                   cudaStream_t s);
+size_t scan_scratch_bytes(int64_t n);
+
+cudaError_t launch_bin(const BinHeader &bh, void *d_bins, const KDesc *kd, const float4 *pts,
+                       double pitch, int64_t n_h, double z_min, double dz, int n_depth, cudaStream_t s);
+
+cudaError_t launch_superpose_v1(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x,
+                                int tiles_y, int64_t row0, int64_t n_h, float2 *psi, cudaStream_t s);
+cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStream_t s);
+
+cudaError_t launch_inverse(const float2 *psi, float2 *u, int64_t rows, int64_t n_h, int64_t row0, int levels,
+                           const double *print4 /* xr, yr, zr, inv_lambda or NULL */, double pitch,
+                           uint8_t *bits, cudaStream_t s);
+cudaError_t launch_quantize(const float2 *u, int64_t rows, int64_t n_h, int64_t row0, const double *print4,
+                            double pitch, uint8_t *bits, cudaStream_t s);
+
+}  // namespace wasabi

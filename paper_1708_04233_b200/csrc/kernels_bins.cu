@@ -1,0 +1,244 @@
+// kernels_bins.cu -- step 2a of WASABI: point conversion and the tile-binning counting sort
+// (the paper re-bases all points per N_h x N_h sub-hologram; here every point
+// is listed in the T x T tiles its PSF footprint overlaps, within the caller's row band).
+//   K3a convert + count (fp64 conversion, R-A3/R-A9/R-A17), K3b scan, K3c scatter (atomic
+//   slots), K3d per-tile sort so each bin lists points in ascending index order (R-A11) --
+//   deterministic bins, and a deterministic per-pixel accumulation order downstream.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace wasabi {
+namespace {
+
+__device__ __forceinline__ long long floor_div(long long a, long long b) {
+    long long q = a / b;
+    if ((a % b != 0) && (a < 0)) q--;
+    return q;
+}
+
+struct BinArgs {
+    int64_t n;
+    int64_t n_h, row0, row1;
+    int T, tiles_x, tiles_y, n_depth;
+    double pitch, z_min, dz;
+};
+
+// Per-point conversion (fp64, same IEEE sequence as the specification):
+//   ix = floor(x/p + 1/2) + N_h/2, iy likewise (R-A9);
+//   t = (z - z_min)/dz, valid iff -1/2 <= t <= N_z - 1/2, iz = clamp(ceil(t - 1/2)) (R-A3, R-A17);
+//   a must be finite and > 0.
+__device__ __forceinline__ bool convert_point(const float4 p, const BinArgs &A, int &ix, int &iy, int &iz) {
+    if (!isfinite(p.x) || !isfinite(p.y) || !isfinite(p.z) || !isfinite(p.w) || !(p.w > 0.0f)) return false;
+    const double u = (double)p.x / A.pitch, v = (double)p.y / A.pitch;
+    if (!(fabs(u) <= 1073741824.0) || !(fabs(v) <= 1073741824.0)) return false;
+    ix = (int)((long long)floor(u + 0.5) + A.n_h / 2);
+    iy = (int)((long long)floor(v + 0.5) + A.n_h / 2);
+    if (A.n_depth <= 1) { iz = 0; return true; }
+    const double t = ((double)p.z - A.z_min) / A.dz;
+    if (t < -0.5 || t > (double)(A.n_depth - 1) + 0.5) return false;
+    long long q = (long long)ceil(t - 0.5);
+    if (q < 0) q = 0;
+    if (q > A.n_depth - 1) q = A.n_depth - 1;
+    iz = (int)q;
+    return true;
+}
+
+// Tile range of a point's footprint box [ix-E, ix+E] x [iy-E, iy+E] within the band.
+__device__ __forceinline__ void tile_range(int ix, int iy, int E, const BinArgs &A, int &tx0, int &tx1, int &ty0,
+                                           int &ty1) {
+    tx0 = (int)max(0LL, floor_div((long long)ix - E, A.T));
+    tx1 = (int)min((long long)A.tiles_x - 1, floor_div((long long)ix + E, A.T));
+    ty0 = (int)max(0LL, floor_div((long long)iy - E - A.row0, A.T));
+    ty1 = (int)min((long long)A.tiles_y - 1, floor_div((long long)iy + E - A.row0, A.T));
+}
+
+__global__ void __launch_bounds__(256) convert_count_kernel(const float4 *__restrict__ pts, BinArgs A,
+                                                            const KDesc *__restrict__ kd, int4 *__restrict__ pout,
+                                                            uint32_t *__restrict__ cnt, BinHeader *bh) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool valid = false;
+    if (j < A.n) {
+        const float4 p = pts[j];
+        int ix = 0, iy = 0, iz = 0;
+        valid = convert_point(p, A, ix, iy, iz);
+        pout[j] = make_int4(ix, iy, valid ? iz : -1, __float_as_int(p.w));
+        if (valid) {
+            int tx0, tx1, ty0, ty1;
+            tile_range(ix, iy, kd[iz].E, A, tx0, tx1, ty0, ty1);
+            for (int ty = ty0; ty <= ty1; ty++)
+                for (int tx = tx0; tx <= tx1; tx++) atomicAdd(&cnt[(int64_t)ty * A.tiles_x + tx], 1u);
+        }
+    }
+    const unsigned vb = __ballot_sync(0xffffffffu, valid);
+    const unsigned ib = __ballot_sync(0xffffffffu, j < A.n && !valid);
+    if ((threadIdx.x & 31) == 0) {
+        if (vb) atomicAdd(&bh->n_valid, (unsigned long long)__popc(vb));
+        if (ib) atomicAdd(&bh->n_skipped, (unsigned long long)__popc(ib));
+    }
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(BinArgs A, const KDesc *__restrict__ kd,
+                                                      const int4 *__restrict__ pconv,
+                                                      const unsigned long long *__restrict__ ptr,
+                                                      uint32_t *__restrict__ fill, uint32_t *__restrict__ idx) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= A.n) return;
+    const int4 q = pconv[j];
+    if (q.z < 0) return;
+    int tx0, tx1, ty0, ty1;
+    tile_range(q.x, q.y, kd[q.z].E, A, tx0, tx1, ty0, ty1);
+    for (int ty = ty0; ty <= ty1; ty++)
+        for (int tx = tx0; tx <= tx1; tx++) {
+            const int64_t t = (int64_t)ty * A.tiles_x + tx;
+            const uint32_t slot = atomicAdd(&fill[t], 1u);
+            idx[ptr[t] + slot] = (uint32_t)j;
+        }
+}
+
+// Warp-per-tile bitonic sort for bins of <= 1024 entries; larger bins are queued.
+constexpr int kSmallBin = 1024;
+__global__ void __launch_bounds__(256) sort_small_kernel(int64_t n_tiles, const unsigned long long *__restrict__ ptr,
+                                                         uint32_t *__restrict__ idx, uint32_t *__restrict__ big_list,
+                                                         unsigned int *big_count) {
+    __shared__ uint32_t sh[8][kSmallBin];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * 8 + w;
+    if (t >= n_tiles) return;
+    const unsigned long long b = ptr[t], e = ptr[t + 1];
+    const int n = (int)(e - b);
+    if (n <= 1) return;
+    if (n > kSmallBin) {
+        if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)t;
+        return;
+    }
+    int m = 2;
+    while (m < n) m <<= 1;
+    uint32_t *s = sh[w];
+    for (int i = lane; i < m; i += 32) s[i] = i < n ? idx[b + i] : 0xffffffffu;
+    __syncwarp();
+    for (int k = 2; k <= m; k <<= 1)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int i = lane; i < m; i += 32) {
+                const int l = i ^ jj;
+                if (l > i) {
+                    const uint32_t x = s[i], y = s[l];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) { s[i] = y; s[l] = x; }
+                }
+            }
+            __syncwarp();
+        }
+    for (int i = lane; i < n; i += 32) idx[b + i] = s[i];
+}
+
+// Large bins: one CTA per queued tile; 4096-entry chunks sorted in shared memory, then merge
+// passes (each element's output rank = own index + lower_bound in the partner run; indices are
+// unique) ping-ponging between idx and idx2.
+constexpr int kChunk = 4096;
+__global__ void __launch_bounds__(512) sort_large_kernel(const unsigned long long *__restrict__ ptr,
+                                                         uint32_t *idx, uint32_t *idx2,
+                                                         const uint32_t *__restrict__ big_list,
+                                                         const unsigned int *__restrict__ big_count) {
+    __shared__ uint32_t s[kChunk];
+    const unsigned nb = *big_count;
+    for (unsigned bi = blockIdx.x; bi < nb; bi += gridDim.x) {
+        const int64_t t = big_list[bi];
+        const unsigned long long b = ptr[t];
+        const int64_t n = (int64_t)(ptr[t + 1] - b);
+        uint32_t *src = idx + b, *dst = idx2 + b;
+        for (int64_t c0 = 0; c0 < n; c0 += kChunk) {
+            const int cn = (int)((n - c0) < kChunk ? (n - c0) : kChunk);
+            int m = 2;
+            while (m < cn) m <<= 1;
+            for (int i = threadIdx.x; i < m; i += blockDim.x) s[i] = i < cn ? src[c0 + i] : 0xffffffffu;
+            __syncthreads();
+            for (int k = 2; k <= m; k <<= 1)
+                for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                        const int l = i ^ jj;
+                        if (l > i) {
+                            const uint32_t x = s[i], y = s[l];
+                            const bool up = (i & k) == 0;
+                            if ((x > y) == up) { s[i] = y; s[l] = x; }
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (int i = threadIdx.x; i < cn; i += blockDim.x) src[c0 + i] = s[i];
+            __syncthreads();
+        }
+        for (int64_t wdt = kChunk; wdt < n; wdt <<= 1) {
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                const int64_t run = i / wdt, r0 = run * wdt, own = i - r0;
+                const bool left = (run & 1) == 0;
+                const int64_t p0 = left ? r0 + wdt : r0 - wdt;           // partner run start
+                const int64_t p1 = min(p0 + wdt, n);
+                const int64_t out0 = left ? r0 : p0;                      // merged block start
+                const uint32_t x = src[i];
+                int64_t lo = p0, hi = p0 < n ? p1 : p0;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (src[mid] < x) lo = mid + 1; else hi = mid;
+                }
+                dst[out0 + own + (lo - p0)] = x;
+            }
+            __syncthreads();
+            uint32_t *tmp = src; src = dst; dst = tmp;
+        }
+        if (src != idx + b)
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) idx[b + i] = src[i];
+        __syncthreads();
+    }
+}
+
+__global__ void finish_kernel(BinHeader *bh, const unsigned long long *ptr, int64_t n_tiles) {
+    bh->total_entries = ptr[n_tiles];
+    if (ptr[n_tiles] > (unsigned long long)bh->capacity) bh->status = 1;
+}
+
+}  // namespace
+
+cudaError_t launch_bin(const BinHeader &h, void *d_bins, const KDesc *kd, const float4 *pts, double pitch,
+                       int64_t n_h, double z_min, double dz, int n_depth, cudaStream_t s) {
+    char *base = reinterpret_cast<char *>(d_bins);
+    BinHeader *bh = reinterpret_cast<BinHeader *>(base);
+    int4 *pconv = reinterpret_cast<int4 *>(base + h.pts_off);
+    unsigned long long *ptr = reinterpret_cast<unsigned long long *>(base + h.ptr_off);
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(base + h.cnt_off);
+    uint32_t *idx = reinterpret_cast<uint32_t *>(base + h.idx_off);
+    uint32_t *idx2 = reinterpret_cast<uint32_t *>(base + h.idx2_off);
+    void *scan_scratch = base + h.scan_off;
+    // the big-bin queue lives after the scan scratch
+    uint32_t *big_list = reinterpret_cast<uint32_t *>(base + h.scan_off + scan_scratch_bytes(h.n_tiles + 1));
+    unsigned int *big_count = reinterpret_cast<unsigned int *>(big_list + h.n_tiles);
+
+    BinArgs A;
+    A.n = h.n_points; A.n_h = n_h; A.row0 = h.row0; A.row1 = h.row1;
+    A.T = h.T; A.tiles_x = h.tiles_x; A.tiles_y = h.tiles_y; A.n_depth = n_depth;
+    A.pitch = pitch; A.z_min = z_min; A.dz = dz;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(h.n_tiles + 1), s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(big_count, 0, sizeof(unsigned int), s)) != cudaSuccess) return e;
+    const unsigned pb = (unsigned)((h.n_points + 255) / 256);
+    if (h.n_points > 0) {
+        count_launches(1);
+        convert_count_kernel<<<pb, 256, 0, s>>>(pts, A, kd, pconv, cnt, bh);
+    }
+    if ((e = launch_scan_u32_to_u64(cnt, ptr, h.n_tiles + 1, scan_scratch, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(h.n_tiles + 1), s)) != cudaSuccess) return e;
+    if (h.n_points > 0) {
+        count_launches(1);
+        scatter_kernel<<<pb, 256, 0, s>>>(A, kd, pconv, ptr, cnt, idx);
+    }
+    count_launches(1);
+    sort_small_kernel<<<(unsigned)((h.n_tiles + 7) / 8), 256, 0, s>>>(h.n_tiles, ptr, idx, big_list, big_count);
+    count_launches(1);
+    sort_large_kernel<<<148 * 2, 512, 0, s>>>(ptr, idx, idx2, big_list, big_count);
+    count_launches(1);
+    finish_kernel<<<1, 1, 0, s>>>(bh, ptr, h.n_tiles);
+    return cudaGetLastError();
+}
+
+}  // namespace wasabi

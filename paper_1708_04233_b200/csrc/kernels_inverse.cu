@@ -1,0 +1,155 @@
+// kernels_inverse.cu -- steps 3 and 4 of WASABI.
+//  K5 inverse_kernel: L-level inverse Haar of one 64 x 64 tile in shared
+//     memory (tile and band edges are multiples of 2^L, so every block is self-contained: no halo),
+//     butterflies a=((LL+HL)+(LH+HH))/2, b=((LL-HL)+(LH-HH))/2, c=((LL+HL)-(LH+HH))/2,
+//     d=((LL-HL)-(LH-HH))/2 (R-A6); optionally fused with the print quantisation.
+//  K6 quantize_kernel: standalone step 4 on an existing u.
+// Step 4 (R-A14, R-A15): I = Re(u conj(R)), R = exp(i k r),
+//     r = sqrt((x-x_r)^2 + (y-y_r)^2 + z_r^2); the phase is reduced in fp64 (r/lambda up to ~1e6
+//     cycles; fp32 would be off by > 0.2 rad) and only the reduced fraction goes to fp32 sincospi.
+// HBM-bound: 16 B/px (read psi, write u), +0.125 B/px bits.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace wasabi {
+namespace {
+
+struct QArgs {
+    double xr, yr, zr2, inv_lambda, pitch;
+    int64_t half;  // N_h / 2
+};
+
+__device__ __forceinline__ float interference(float2 u, int64_t X, int64_t Y, const QArgs &q) {
+    const double x = (double)(X - q.half) * q.pitch, y = (double)(Y - q.half) * q.pitch;
+    const double dx = x - q.xr, dy = y - q.yr;
+    const double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), q.zr2));
+    const double cyc = r * q.inv_lambda;
+    const float f = (float)(cyc - rint(cyc));  // in [-1/2, 1/2]
+    float s, c;
+    sincospif(2.0f * f, &s, &c);
+    return fmaf(u.x, c, u.y * s);
+}
+
+constexpr int kT = 64;
+constexpr int kS = kT + 2;  // float2 row stride (keeps float4 alignment of rows)
+
+__global__ void __launch_bounds__(256) inverse_kernel(const float2 *psi, float2 *u, int64_t n_h, int64_t row0, int L,
+                                                      QArgs q, uint8_t *__restrict__ bits, int write_u, int do_bits) {
+    __shared__ __align__(16) float2 s[kT * kS];
+    const int64_t X0 = (int64_t)blockIdx.x * kT, Yl0 = (int64_t)blockIdx.y * kT;  // band-local rows
+    const float4 *src = reinterpret_cast<const float4 *>(psi);
+    // load 64 rows x 64 complex (32 float4 per row), coalesced
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        const int f = threadIdx.x + 256 * i;
+        const int row = f >> 5, c4 = f & 31;
+        const float4 v = src[((Yl0 + row) * n_h + X0) / 2 + c4];
+        *reinterpret_cast<float4 *>(&s[row * kS + 2 * c4]) = v;
+    }
+    __syncthreads();
+    for (int l = L; l >= 1; l--) {
+        const int st = 1 << (l - 1), nq = kT >> l;
+        for (int qd = threadIdx.x; qd < nq * nq; qd += 256) {
+            const int bx = (qd % nq) << l, by = (qd / nq) << l;
+            float2 *pa = &s[by * kS + bx], *pb = pa + st, *pc = pa + st * kS, *pd = pc + st;
+            const float2 LL = *pa, HL = *pb, LH = *pc, HH = *pd;
+            float2 A, B, C, D;
+            A.x = ((LL.x + HL.x) + (LH.x + HH.x)) * 0.5f;
+            B.x = ((LL.x - HL.x) + (LH.x - HH.x)) * 0.5f;
+            C.x = ((LL.x + HL.x) - (LH.x + HH.x)) * 0.5f;
+            D.x = ((LL.x - HL.x) - (LH.x - HH.x)) * 0.5f;
+            A.y = ((LL.y + HL.y) + (LH.y + HH.y)) * 0.5f;
+            B.y = ((LL.y - HL.y) + (LH.y - HH.y)) * 0.5f;
+            C.y = ((LL.y + HL.y) - (LH.y + HH.y)) * 0.5f;
+            D.y = ((LL.y - HL.y) - (LH.y - HH.y)) * 0.5f;
+            *pa = A; *pb = B; *pc = C; *pd = D;
+        }
+        __syncthreads();
+    }
+    if (write_u) {
+        float4 *dst = reinterpret_cast<float4 *>(u);
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int f = threadIdx.x + 256 * i;
+            const int row = f >> 5, c4 = f & 31;
+            dst[((Yl0 + row) * n_h + X0) / 2 + c4] = *reinterpret_cast<const float4 *>(&s[row * kS + 2 * c4]);
+        }
+    }
+    if (do_bits) {
+        // 64 rows x 8 bytes per tile; thread -> 2 bytes
+        for (int bi = threadIdx.x; bi < kT * 8; bi += 256) {
+            const int row = bi >> 3, xb = bi & 7;
+            const int64_t Y = row0 + Yl0 + row;
+            unsigned byte = 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int x = xb * 8 + i;
+                const float I = interference(s[row * kS + x], X0 + x, Y, q);
+                byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
+            }
+            bits[(Yl0 + row) * (n_h / 8) + X0 / 8 + xb] = (uint8_t)byte;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) quantize_kernel(const float2 *__restrict__ u, int64_t rows, int64_t n_h,
+                                                       int64_t row0, QArgs q, uint8_t *__restrict__ bits) {
+    const int64_t nbytes = rows * (n_h / 8);
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t yl = b / (n_h / 8), xb = b % (n_h / 8);
+        const float4 *p = reinterpret_cast<const float4 *>(u + yl * n_h + xb * 8);
+        float2 v[8];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const float4 f = p[i];
+            v[2 * i] = make_float2(f.x, f.y);
+            v[2 * i + 1] = make_float2(f.z, f.w);
+        }
+        unsigned byte = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const float I = interference(v[i], xb * 8 + i, row0 + yl, q);
+            byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
+        }
+        bits[b] = (uint8_t)byte;
+    }
+}
+
+QArgs make_q(const double *print4, double pitch, int64_t n_h) {
+    QArgs q;
+    q.xr = print4 ? print4[0] : 0.0;
+    q.yr = print4 ? print4[1] : 0.0;
+    q.zr2 = print4 ? print4[2] * print4[2] : 0.0;
+    q.inv_lambda = print4 ? print4[3] : 0.0;
+    q.pitch = pitch;
+    q.half = n_h / 2;
+    return q;
+}
+
+}  // namespace
+
+cudaError_t launch_inverse(const float2 *psi, float2 *u, int64_t rows, int64_t n_h, int64_t row0, int levels,
+                           const double *print4, double pitch, uint8_t *bits, cudaStream_t s) {
+    const QArgs q = make_q(print4, pitch, n_h);
+    dim3 grid((unsigned)(n_h / kT), (unsigned)(rows / kT));
+    if (grid.x == 0 || grid.y == 0) return cudaSuccess;
+    count_launches(1);
+    inverse_kernel<<<grid, 256, 0, s>>>(psi, u, n_h, row0, levels, q, bits, u != nullptr, bits != nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const float2 *u, int64_t rows, int64_t n_h, int64_t row0, const double *print4,
+                            double pitch, uint8_t *bits, cudaStream_t s) {
+    const QArgs q = make_q(print4, pitch, n_h);
+    const int64_t nbytes = rows * (n_h / 8);
+    if (nbytes == 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>((nbytes + 255) / 256, 148 * 64);
+    count_launches(1);
+    quantize_kernel<<<(unsigned)blocks, 256, 0, s>>>(u, rows, n_h, row0, q, bits);
+    return cudaGetLastError();
+}
+
+}  // namespace wasabi

@@ -1,0 +1,275 @@
+// kernels_tables.cu -- step 1 of WASABI: per-depth PSF, forward Haar, top-N_r
+// selection and the LUT with its per-level band index.  Compiled with --fmad=false and explicit
+// _rn intrinsics on the key path so that the fp32 rank keys are computed with the same IEEE
+// operation sequence as the specification (K1/K2).  Off the per-frame hot loop:
+// one launch set per parameter set.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace wasabi {
+namespace {
+
+__device__ __forceinline__ const TableHeader &hdr(const void *t) {
+    return *reinterpret_cast<const TableHeader *>(t);
+}
+template <typename T>
+__device__ __forceinline__ const T *at(const void *t, int64_t off) {
+    return reinterpret_cast<const T *>(reinterpret_cast<const char *>(t) + off);
+}
+template <typename T>
+__device__ __forceinline__ T *atw(void *t, int64_t off) {
+    return reinterpret_cast<T *>(reinterpret_cast<char *>(t) + off);
+}
+
+// CTA -> depth: largest d with cta_base[d] <= b (cta_base has n_depth + 1 entries).
+__device__ __forceinline__ int find_depth(const int32_t *base, int n, int64_t b) {
+    int lo = 0, hi = n;  // invariant base[lo] <= b < base[hi]
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (base[mid] <= b) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+constexpr int kTile = 64;
+
+// K1: one CTA per 64x64 region of one depth table.  PSF u_z = exp(i k r) circ(.) with r =
+// sqrt((dx p)^2 + (dy p)^2 + z^2), support S = {dx^2+dy^2 < R^2} U {0}
+// (R-A2), then L forward Haar levels in shared memory in fp64 with the butterfly order
+// LL=((a+b)+(c+d))/2, HL=((a-b)+(c-d))/2, LH=((a+b)-(c+d))/2, HH=((a-b)-(c-d))/2 (R-A6).
+// Output: fp32 value and the rank key bits of fp32_RN(re^2 + im^2) (R-A13).
+__global__ void __launch_bounds__(256) psf_haar_kernel(const void *tables, float2 *__restrict__ coef_val,
+                                                       uint32_t *__restrict__ coef_key, double k, double pitch,
+                                                       int L, int n_depth) {
+    extern __shared__ double2 f[];  // 64 x 64
+    const TableHeader &h = hdr(tables);
+    const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
+    const int32_t *cbase = at<int32_t>(tables, h.ctabase_off);
+    const int d = find_depth(cbase, n_depth, blockIdx.x);
+    const DDesc D = dd[d];
+    const int local = (int)blockIdx.x - D.cta_base;
+    const int X0 = (local % D.tiles) * kTile, Y0 = (local / D.tiles) * kTile;
+    const int side = D.side, H = side >> 1;
+    const double R2 = __dmul_rn(D.R, D.R);
+    const double z2 = __dmul_rn(D.z, D.z);
+
+    for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
+        const int x = i & (kTile - 1), y = i >> 6;
+        const int X = X0 + x, Y = Y0 + y;
+        double2 v = make_double2(0.0, 0.0);
+        if (X < side && Y < side) {
+            const long long dx = X - H, dy = Y - H;
+            const bool in = (dx == 0 && dy == 0) || ((double)(dx * dx + dy * dy) < R2);
+            if (in) {
+                const double xp = __dmul_rn((double)dx, pitch), yp = __dmul_rn((double)dy, pitch);
+                const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xp, xp), __dmul_rn(yp, yp)), z2));
+                double s, c;
+                sincos(__dmul_rn(k, r), &s, &c);
+                v = make_double2(c, s);
+            }
+        }
+        f[i] = v;
+    }
+    __syncthreads();
+    for (int l = 1; l <= L; l++) {
+        const int bs = 1 << l, st = bs >> 1, nqs = kTile >> l;
+        for (int q = threadIdx.x; q < nqs * nqs; q += blockDim.x) {
+            const int bx = (q % nqs) << l, by = (q / nqs) << l;
+            double2 *pa = &f[by * kTile + bx], *pb = pa + st, *pc = pa + st * kTile, *pd = pc + st;
+            const double2 a = *pa, b = *pb, c = *pc, e = *pd;
+            double2 LL, HL, LH, HH;
+            LL.x = __dadd_rn(__dadd_rn(a.x, b.x), __dadd_rn(c.x, e.x)) * 0.5;
+            HL.x = __dadd_rn(__dsub_rn(a.x, b.x), __dsub_rn(c.x, e.x)) * 0.5;
+            LH.x = __dsub_rn(__dadd_rn(a.x, b.x), __dadd_rn(c.x, e.x)) * 0.5;
+            HH.x = __dsub_rn(__dsub_rn(a.x, b.x), __dsub_rn(c.x, e.x)) * 0.5;
+            LL.y = __dadd_rn(__dadd_rn(a.y, b.y), __dadd_rn(c.y, e.y)) * 0.5;
+            HL.y = __dadd_rn(__dsub_rn(a.y, b.y), __dsub_rn(c.y, e.y)) * 0.5;
+            LH.y = __dsub_rn(__dadd_rn(a.y, b.y), __dadd_rn(c.y, e.y)) * 0.5;
+            HH.y = __dsub_rn(__dsub_rn(a.y, b.y), __dsub_rn(c.y, e.y)) * 0.5;
+            *pa = LL; *pb = HL; *pc = LH; *pd = HH;
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
+        const int x = i & (kTile - 1), y = i >> 6;
+        const int X = X0 + x, Y = Y0 + y;
+        if (X < side && Y < side) {
+            const double2 v = f[i];
+            const int64_t o = D.coef_off + (int64_t)Y * side + X;
+            coef_val[o] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+            const double m2 = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+            coef_key[o] = __float_as_uint(__double2float_rn(m2));
+        }
+    }
+}
+
+// Selection state per depth: {prefix, mask, remaining k} of the composite 64-bit key
+// (kappa_bits << 32) | ~linear_index: larger key = larger |c|^2, then smaller index (R-A13).
+struct SelState {
+    unsigned long long prefix, mask, k;
+};
+
+// K2a: radix-select histogram pass (8 passes of 8 bits, MSB first) over keys matching the prefix.
+__global__ void __launch_bounds__(256) select_hist_kernel(const void *tables, const uint32_t *__restrict__ coef_key,
+                                                          unsigned int *__restrict__ hist,
+                                                          const SelState *__restrict__ st, int n_depth, int pass) {
+    __shared__ unsigned int sh[256];
+    const TableHeader &h = hdr(tables);
+    const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
+    const int32_t *cbase = at<int32_t>(tables, h.ctabase_off);
+    const int d = find_depth(cbase, n_depth, blockIdx.x);
+    const DDesc D = dd[d];
+    const int local = (int)blockIdx.x - D.cta_base;
+    const int X0 = (local % D.tiles) * kTile, Y0 = (local / D.tiles) * kTile;
+    const int side = D.side;
+    const SelState s = st[d];
+    const int shift = 56 - 8 * pass;
+    sh[threadIdx.x] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kTile * kTile; i += blockDim.x) {
+        const int X = X0 + (i & (kTile - 1)), Y = Y0 + (i >> 6);
+        if (X < side && Y < side) {
+            const uint32_t lin = (uint32_t)(Y * side + X);
+            const unsigned long long key = ((unsigned long long)coef_key[D.coef_off + (int64_t)Y * side + X] << 32) |
+                                           (unsigned long long)(~lin);
+            if ((key & s.mask) == s.prefix) atomicAdd(&sh[(key >> shift) & 255u], 1u);
+        }
+    }
+    __syncthreads();
+    const unsigned int c = sh[threadIdx.x];
+    if (c) atomicAdd(&hist[d * 256 + threadIdx.x], c);
+}
+
+// K2b: per depth, choose the digit containing the k-th largest key; zero the histogram.
+__global__ void select_pick_kernel(unsigned int *hist, SelState *st, int n_depth, int pass) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_depth) return;
+    SelState s = st[d];
+    const int shift = 56 - 8 * pass;
+    unsigned long long cum = 0;
+    int digit = 0;
+    for (int b = 255; b >= 0; b--) {
+        const unsigned long long c = hist[d * 256 + b];
+        if (cum + c >= s.k) { digit = b; break; }
+        cum += c;
+    }
+    s.k -= cum;
+    s.prefix |= (unsigned long long)digit << shift;
+    s.mask |= 0xFFull << shift;
+    st[d] = s;
+    for (int b = 0; b < 256; b++) hist[d * 256 + b] = 0;
+}
+
+__global__ void select_init_kernel(const void *tables, SelState *st, int n_depth) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_depth) return;
+    const TableHeader &h = hdr(tables);
+    const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
+    st[d].prefix = 0;
+    st[d].mask = 0;
+    st[d].k = (unsigned long long)dd[d].n_r;
+}
+
+// K2c: per (depth, level, band, Xb) group, count (pass 0) or scatter (pass 1) the kept
+// coefficients in (Yb, subband) order.  Entry record: value float2 + packed position
+// pos = w | (u << 16), u = 2 (Yb - band hb) + sby, v = 2 Xb + sbx, w = u S + v.
+__global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 *__restrict__ coef_val,
+                                                     const uint32_t *__restrict__ coef_key,
+                                                     const SelState *__restrict__ st, int n_depth, int L, int T,
+                                                     int pass) {
+    const TableHeader &h = hdr(tables);
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= h.total_ptrs) return;
+    const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
+    const KDesc *kd = at<KDesc>(tables, h.kdesc_off);
+    int32_t *ptr = atw<int32_t>(tables, h.ptr_off);
+    // depth: largest d with group_base <= g
+    int lo = 0, hi = n_depth;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (dd[mid].group_base <= g) lo = mid; else hi = mid;
+    }
+    const int d = lo;
+    const DDesc D = dd[d];
+    const KDesc K = kd[d];
+    int l = 1;
+    while (l < L && K.ptr_base[l] <= g) l++;
+    const int side = D.side;
+    const int nb = side >> l, hb = band_blocks(T, l);
+    const int64_t local = g - K.ptr_base[l - 1];
+    const int band = (int)(local / (nb + 1)), Xb = (int)(local % (nb + 1));
+    if (Xb == nb) {  // dummy slot: band end
+        if (pass == 0) ptr[g] = 0;
+        return;
+    }
+    const unsigned long long thr = st[d].prefix;
+    const int st_px = 1 << (l - 1);
+    const int yb1 = min(band * hb + hb, nb);
+    const int S = h.S;
+    int out = pass ? ptr[g] : 0;
+    int cnt = 0;
+    float2 *val = atw<float2>(tables, h.val_off);
+    uint32_t *pos = atw<uint32_t>(tables, h.pos_off);
+    for (int Yb = band * hb; Yb < yb1; Yb++) {
+        for (int sb = (l == L ? 0 : 1); sb < 4; sb++) {
+            const int sbx = sb & 1, sby = sb >> 1;
+            const int X = (Xb << l) + sbx * st_px, Y = (Yb << l) + sby * st_px;
+            const uint32_t lin = (uint32_t)(Y * side + X);
+            const int64_t o = D.coef_off + (int64_t)Y * side + X;
+            const unsigned long long key = ((unsigned long long)coef_key[o] << 32) | (unsigned long long)(~lin);
+            if (key >= thr) {
+                if (pass) {
+                    const int u = 2 * (Yb - band * hb) + sby, v = 2 * Xb + sbx;
+                    val[out] = coef_val[o];
+                    pos[out] = (uint32_t)(u * S + v) | ((uint32_t)u << 16);
+                    out++;
+                }
+                cnt++;
+            }
+        }
+    }
+    (void)K;
+    if (pass == 0) ptr[g] = cnt;
+}
+
+}  // namespace
+
+cudaError_t launch_psf_haar(const TableHeader &h, const void *d_tables, float2 *coef_val, uint32_t *coef_key,
+                            double k, double pitch, int levels, int n_depth, cudaStream_t s) {
+    const int smem = kTile * kTile * sizeof(double2);
+    cudaError_t e = cudaFuncSetAttribute(psf_haar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    count_launches(1);
+    psf_haar_kernel<<<(unsigned)h.total_ctas, 256, smem, s>>>(d_tables, coef_val, coef_key, k, pitch, levels,
+                                                              n_depth);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select(const TableHeader &h, const void *d_tables, const uint32_t *coef_key, unsigned int *hist,
+                          unsigned long long *sel_state, int n_depth, cudaStream_t s) {
+    SelState *st = reinterpret_cast<SelState *>(sel_state);
+    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned int) * 256 * (size_t)n_depth, s);
+    if (e != cudaSuccess) return e;
+    count_launches(1);
+    select_init_kernel<<<(n_depth + 127) / 128, 128, 0, s>>>(d_tables, st, n_depth);
+    for (int pass = 0; pass < 8; pass++) {
+        count_launches(1);
+        select_hist_kernel<<<(unsigned)h.total_ctas, 256, 0, s>>>(d_tables, coef_key, hist, st, n_depth, pass);
+        count_launches(1);
+        select_pick_kernel<<<(n_depth + 127) / 128, 128, 0, s>>>(hist, st, n_depth, pass);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_groups(const TableHeader &h, void *d_tables, const float2 *coef_val, const uint32_t *coef_key,
+                          const unsigned long long *sel_state, int pass, cudaStream_t s) {
+    const SelState *st = reinterpret_cast<const SelState *>(sel_state);
+    const unsigned blocks = (unsigned)((h.total_ptrs + 255) / 256);
+    count_launches(1);
+    groups_kernel<<<blocks, 256, 0, s>>>(d_tables, coef_val, coef_key, st, h.n_depth, h.levels, h.tile, pass);
+    return cudaGetLastError();
+}
+
+}  // namespace wasabi

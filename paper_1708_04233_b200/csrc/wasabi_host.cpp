@@ -1,0 +1,575 @@
+// wasabi_host.cpp -- the C ABI (include/wasabi.h): parameter validation, host-side geometry (L0),
+// device buffer layouts, and the kernel launch sequence of every step.  No device memory is
+// allocated here; every buffer belongs to the caller.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "wasabi.h"
+#include "internal.h"
+
+#include <atomic>
+
+using namespace wasabi;
+
+namespace wasabi {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+}  // namespace wasabi
+
+namespace {
+
+thread_local std::string g_err;
+
+wasabi_status fail(wasabi_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+wasabi_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(WASABI_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                   \
+    do {                                                 \
+        cudaError_t _e = (expr);                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, what); \
+    } while (0)
+
+constexpr double kPi = 3.14159265358979323846;
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+uint64_t fnv(uint64_t h, const void *p, size_t n) {
+    const unsigned char *c = static_cast<const unsigned char *>(p);
+    for (size_t i = 0; i < n; i++) { h ^= c[i]; h *= 1099511628211ull; }
+    return h;
+}
+
+uint64_t param_hash(const wasabi_params &P) {
+    uint64_t h = 1469598103934665603ull;
+    h = fnv(h, &P.wavelength_m, 8); h = fnv(h, &P.pitch_m, 8); h = fnv(h, &P.n_h, 8);
+    h = fnv(h, &P.n_depth, 4); h = fnv(h, &P.levels, 4); h = fnv(h, &P.z_min_m, 8);
+    h = fnv(h, &P.z_max_m, 8); h = fnv(h, &P.retention, 8); h = fnv(h, &P.tile, 4);
+    return h;
+}
+
+wasabi_status validate(const wasabi_params *P) {
+    if (!P) return fail(WASABI_EINVAL, "params is NULL");
+    if (!(P->wavelength_m > 0) || !std::isfinite(P->wavelength_m)) return fail(WASABI_EINVAL, "wavelength_m must be > 0");
+    if (!(P->pitch_m > 0) || !std::isfinite(P->pitch_m)) return fail(WASABI_EINVAL, "pitch_m must be > 0");
+    if (!(P->wavelength_m < 2.0 * P->pitch_m))
+        return fail(WASABI_EINVAL, "Nyquist: wavelength (%g) must be < 2 * pitch (%g)", P->wavelength_m, P->pitch_m);
+    if (P->levels < 1 || P->levels > kMaxLevels) return fail(WASABI_EINVAL, "levels must be in 1..%d", kMaxLevels);
+    if (P->tile != 64 && P->tile != 128) return fail(WASABI_EINVAL, "tile must be 64 or 128 (shared-memory tile)");
+    if (P->tile % (1 << P->levels)) return fail(WASABI_EINVAL, "tile must be a multiple of 2^levels");
+    if (P->n_h <= 0 || P->n_h % P->tile) return fail(WASABI_EINVAL, "n_h (%lld) must be a positive multiple of tile",
+                                                     (long long)P->n_h);
+    if (P->n_h > (1ll << 24)) return fail(WASABI_EINVAL, "n_h too large");
+    if (P->n_depth < 1) return fail(WASABI_EINVAL, "n_depth must be >= 1");
+    if (!std::isfinite(P->z_min_m) || !std::isfinite(P->z_max_m) || P->z_max_m < P->z_min_m)
+        return fail(WASABI_EINVAL, "need finite z_min <= z_max");
+    if (P->n_depth > 1 && !(P->z_max_m > P->z_min_m)) return fail(WASABI_EINVAL, "n_depth > 1 needs z_max > z_min");
+    if (!(P->retention > 0) || P->retention > 1) return fail(WASABI_EINVAL, "retention must be in (0, 1]");
+    if (llround(P->retention * 1e6) < 1) return fail(WASABI_EINVAL, "retention below 1 ppm");
+    if (P->flags != 0) return fail(WASABI_EINVAL, "flags must be 0");
+    return WASABI_OK;
+}
+
+wasabi_status validate_band(const wasabi_params *P, int64_t row0, int64_t row1) {
+    if (row0 < 0 || row1 > P->n_h || row0 > row1) return fail(WASABI_EINVAL, "band [%lld, %lld) outside [0, n_h)",
+                                                              (long long)row0, (long long)row1);
+    if (row0 % P->tile || row1 % P->tile) return fail(WASABI_EINVAL, "band rows must be multiples of tile");
+    return WASABI_OK;
+}
+
+// S_d membership (PAPER.md:90 circ, centre always kept).
+inline bool in_support(int64_t dx, int64_t dy, double R) {
+    if (dx == 0 && dy == 0) return true;
+    return (double)(dx * dx + dy * dy) < R * R;
+}
+
+// Structural nnz: coefficient positions whose support block touches S_d.  Per block row the
+// disc's x-extent is the union of symmetric row intervals [-xm, xm], so the blocks touched are
+// those overlapping [H - max xm, H + max xm].
+int64_t nnz_structural(int64_t H, double R, int L) {
+    const int64_t side = 2 * H;
+    std::vector<int64_t> xm(side);
+    for (int64_t Y = 0; Y < side; Y++) {
+        const int64_t dy = Y - H;
+        const double s = R * R - (double)(dy * dy);
+        int64_t x = s > 0 ? (int64_t)std::floor(std::sqrt(s)) : 0;
+        while (x >= 0 && !in_support(x, dy, R)) x--;
+        while (x >= 0 && in_support(x + 1, dy, R)) x++;
+        xm[Y] = x;  // -1: row empty
+    }
+    int64_t nnz = 0;
+    for (int l = 1; l <= L; l++) {
+        const int64_t b = 1ll << l;
+        for (int64_t Y0 = 0; Y0 < side; Y0 += b) {
+            int64_t X = -1;
+            for (int64_t Y = Y0; Y < Y0 + b; Y++) X = std::max(X, xm[Y]);
+            if (X < 0) continue;
+            const int64_t nblk = (H + X) / b - (H - X) / b + 1;
+            nnz += nblk * (l == L ? 4 : 3);
+        }
+    }
+    return nnz;
+}
+
+struct Geo {
+    wasabi_params P;
+    double k, tan_theta, dz;
+    int T, S, L, nd;
+    std::vector<KDesc> kd;
+    std::vector<DDesc> dd;
+    std::vector<int32_t> ctabase;
+    int64_t total_entries = 0, total_ptrs = 0, total_ctas = 0, total_coef = 0, max_E = 0;
+    TableHeader th;
+    size_t table_bytes = 0, scratch_bytes = 0;
+    size_t sc_val = 0, sc_key = 0, sc_hist = 0, sc_sel = 0, sc_scan = 0;
+};
+
+double level_z(const wasabi_params &P, double dz, int d) {
+    if (P.n_depth <= 1) return P.z_min_m;
+    return P.z_min_m + (double)d * dz;
+}
+
+wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
+    wasabi_status st = validate(P);
+    if (st != WASABI_OK) return st;
+    g.P = *P;
+    g.T = P->tile; g.S = P->tile + 1; g.L = P->levels; g.nd = P->n_depth;
+    g.k = 2.0 * kPi / P->wavelength_m;
+    const double sigma = P->wavelength_m / (2.0 * P->pitch_m);
+    g.tan_theta = sigma / std::sqrt(1.0 - sigma * sigma);
+    g.dz = P->n_depth > 1 ? (P->z_max_m - P->z_min_m) / (double)(P->n_depth - 1) : 0.0;
+    g.kd.assign(g.nd, KDesc{});
+    g.dd.assign(g.nd, DDesc{});
+    g.ctabase.assign(g.nd + 1, 0);
+    const int64_t B = 1ll << g.L;
+    int64_t ptr = 0, ctas = 0, coef = 0, entries = 0;
+    for (int d = 0; d < g.nd; d++) {
+        const double z = level_z(*P, g.dz, d);
+        const double R = std::fabs(z) * g.tan_theta / P->pitch_m;
+        const int64_t H = B * ((int64_t)std::floor(R / (double)B) + 1);
+        if (2 * H > kMaxTableSide)
+            return fail(WASABI_EINVAL, "depth %d: PSF table side %lld exceeds %d (|z| too large for this pitch)", d,
+                        (long long)(2 * H), kMaxTableSide);
+        const int64_t E = (int64_t)std::ceil(R) + 3 * (1ll << (g.L - 1));
+        DDesc &D = g.dd[d];
+        KDesc &K = g.kd[d];
+        D.z = z; D.R = R;
+        D.side = (int32_t)(2 * H);
+        D.tiles = (int32_t)((2 * H + 63) / 64);
+        D.cta_base = (int32_t)ctas;
+        g.ctabase[d] = (int32_t)ctas;
+        ctas += (int64_t)D.tiles * D.tiles;
+        D.coef_off = coef;
+        coef += 4 * H * H;
+        K.H = (int32_t)H;
+        K.E = (int32_t)E;
+        g.max_E = std::max(g.max_E, E);
+        D.group_base = (int32_t)ptr;
+        for (int l = 1; l <= g.L; l++) {
+            const int64_t nb = (2 * H) >> l, hb = band_blocks(g.T, l), nbands = (nb + hb - 1) / hb;
+            K.ptr_base[l - 1] = (int32_t)ptr;
+            ptr += nbands * (nb + 1);
+        }
+        for (int l = g.L + 1; l <= kMaxLevels; l++) K.ptr_base[l - 1] = (int32_t)ptr;
+        D.n_groups = (int32_t)(ptr - D.group_base);
+        D.nnz = nnz_structural(H, R, g.L);
+        {
+            const int64_t r_ppm = llround(P->retention * 1e6);
+            const int64_t n = (r_ppm * D.nnz + 999999) / 1000000;
+            D.n_r = std::min(n, D.nnz);
+        }
+        entries += D.n_r;
+        if (ptr > (int64_t)INT32_MAX / 2 || entries > (int64_t)INT32_MAX / 2 || ctas > (int64_t)INT32_MAX / 2)
+            return fail(WASABI_EINVAL, "table too large for 32-bit indices");
+    }
+    g.ctabase[g.nd] = (int32_t)ctas;
+    g.total_entries = entries; g.total_ptrs = ptr; g.total_ctas = ctas; g.total_coef = coef;
+    // table buffer layout
+    TableHeader &h = g.th;
+    std::memset(&h, 0, sizeof h);
+    h.magic = kTableMagic;
+    h.param_hash = param_hash(*P);
+    h.n_depth = g.nd; h.levels = g.L; h.tile = g.T; h.S = g.S;
+    h.total_entries = entries; h.total_ptrs = ptr; h.total_ctas = ctas;
+    size_t off = 256;
+    h.kdesc_off = off; off = align_up(off + sizeof(KDesc) * g.nd, 256);
+    h.ddesc_off = off; off = align_up(off + sizeof(DDesc) * g.nd, 256);
+    h.ctabase_off = off; off = align_up(off + 4 * (g.nd + 1), 256);
+    h.ptr_off = off; off = align_up(off + 4 * (size_t)(ptr + 1), 256);
+    h.pos_off = off; off = align_up(off + 4 * (size_t)entries, 256);
+    h.val_off = off; off = align_up(off + 8 * (size_t)entries, 256);
+    h.table_bytes = off;
+    g.table_bytes = off;
+    // build scratch
+    size_t so = 0;
+    g.sc_val = so; so = align_up(so + 8 * (size_t)coef, 256);
+    g.sc_key = so; so = align_up(so + 4 * (size_t)coef, 256);
+    g.sc_hist = so; so = align_up(so + 4 * 256 * (size_t)g.nd, 256);
+    g.sc_sel = so; so = align_up(so + 24 * (size_t)g.nd, 256);
+    g.sc_scan = so; so = align_up(so + scan_scratch_bytes(ptr + 1), 256);
+    g.scratch_bytes = so;
+    return WASABI_OK;
+}
+
+// Bin buffer layout.
+struct BinLayout {
+    BinHeader h;
+    size_t bytes;
+};
+
+BinLayout bin_layout(const Geo &g, int64_t n, int64_t row0, int64_t row1) {
+    BinLayout b;
+    BinHeader &h = b.h;
+    std::memset(&h, 0, sizeof h);
+    h.magic = kBinMagic;
+    h.param_hash = param_hash(g.P);
+    h.n_points = n; h.row0 = row0; h.row1 = row1;
+    h.T = g.T;
+    h.tiles_x = (int32_t)(g.P.n_h / g.T);
+    h.tiles_y = (int32_t)((row1 - row0) / g.T);
+    h.n_tiles = (int64_t)h.tiles_x * h.tiles_y;
+    const int64_t span = (2 * g.max_E) / g.T + 2;
+    const int64_t per_pt = std::min<int64_t>(h.tiles_x, span) * std::min<int64_t>(h.tiles_y, span);
+    h.capacity = n * per_pt;
+    size_t off = 512;
+    h.ptr_off = off; off = align_up(off + 8 * (size_t)(h.n_tiles + 1), 256);
+    h.cnt_off = off; off = align_up(off + 4 * (size_t)(h.n_tiles + 1), 256);
+    h.scan_off = off;
+    off = align_up(off + scan_scratch_bytes(h.n_tiles + 1) + 4 * (size_t)h.n_tiles + 4, 256);
+    h.pts_off = off; off = align_up(off + 16 * (size_t)n, 256);
+    h.idx_off = off; off = align_up(off + 4 * (size_t)h.capacity, 256);
+    h.idx2_off = off; off = align_up(off + 4 * (size_t)h.capacity, 256);
+    h.bin_bytes = off;
+    b.bytes = off;
+    return b;
+}
+
+bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char *wasabi_last_error(void) { return g_err.c_str(); }
+
+const char *wasabi_version(void) { return "wasabi-b200 0.1 (sm_100a)"; }
+
+unsigned long long wasabi_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+wasabi_status wasabi_psf_tables_bytes(const wasabi_params *params, size_t *table_bytes, size_t *scratch_bytes) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if (table_bytes) *table_bytes = g.table_bytes;
+    if (scratch_bytes) *scratch_bytes = g.scratch_bytes;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_depth_geometry(const wasabi_params *params, int32_t depth, wasabi_depth_info *out) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if (depth < 0 || depth >= g.nd || !out) return fail(WASABI_EINVAL, "depth out of range");
+    out->z_m = g.dd[depth].z;
+    out->radius_px = g.dd[depth].R;
+    out->half = g.kd[depth].H;
+    out->footprint = g.kd[depth].E;
+    out->nnz = g.dd[depth].nnz;
+    out->n_r = g.dd[depth].n_r;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_build_psf_tables(const wasabi_params *params, void *d_tables, size_t table_bytes,
+                                      void *d_scratch, size_t scratch_bytes, cudaStream_t stream) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if (!d_tables || !d_scratch) return fail(WASABI_EINVAL, "NULL buffer");
+    if (!aligned(d_tables, 256) || !aligned(d_scratch, 256)) return fail(WASABI_EINVAL, "buffers must be 256-byte aligned");
+    if (table_bytes < g.table_bytes) return fail(WASABI_ENOSPC, "table buffer needs %zu bytes", g.table_bytes);
+    if (scratch_bytes < g.scratch_bytes) return fail(WASABI_ENOSPC, "scratch buffer needs %zu bytes", g.scratch_bytes);
+    char *tb = static_cast<char *>(d_tables);
+    char *sb = static_cast<char *>(d_scratch);
+    CK(launch_write_blob(tb, &g.th, sizeof g.th, stream), "write table header");
+    CK(launch_write_blob(tb + g.th.kdesc_off, g.kd.data(), sizeof(KDesc) * g.nd, stream), "write kdesc");
+    CK(launch_write_blob(tb + g.th.ddesc_off, g.dd.data(), sizeof(DDesc) * g.nd, stream), "write ddesc");
+    CK(launch_write_blob(tb + g.th.ctabase_off, g.ctabase.data(), 4 * (g.nd + 1), stream), "write ctabase");
+    float2 *cval = reinterpret_cast<float2 *>(sb + g.sc_val);
+    uint32_t *ckey = reinterpret_cast<uint32_t *>(sb + g.sc_key);
+    CK(launch_psf_haar(g.th, d_tables, cval, ckey, g.k, params->pitch_m, g.L, g.nd, stream), "psf_haar");
+    CK(launch_select(g.th, d_tables, ckey, reinterpret_cast<unsigned int *>(sb + g.sc_hist),
+                     reinterpret_cast<unsigned long long *>(sb + g.sc_sel), g.nd, stream),
+       "select");
+    CK(cudaMemsetAsync(tb + g.th.ptr_off, 0, 4 * (size_t)(g.total_ptrs + 1), stream), "memset ptr");
+    const unsigned long long *sel = reinterpret_cast<const unsigned long long *>(sb + g.sc_sel);
+    CK(launch_groups(g.th, d_tables, cval, ckey, sel, 0, stream), "groups count");
+    CK(launch_scan_i32(reinterpret_cast<int32_t *>(tb + g.th.ptr_off), g.total_ptrs + 1, sb + g.sc_scan, stream),
+       "scan ptr");
+    CK(launch_groups(g.th, d_tables, cval, ckey, sel, 1, stream), "groups scatter");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_bin_points_bytes(const wasabi_params *params, int64_t n, int64_t row0, int64_t row1,
+                                      size_t *bin_bytes) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(WASABI_EINVAL, "n out of range");
+    if (bin_bytes) *bin_bytes = bin_layout(g, n, row0, row1).bytes;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_tables, const float *d_points, int64_t n,
+                                int64_t row0, int64_t row1, void *d_bins, size_t bin_bytes, cudaStream_t stream) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(WASABI_EINVAL, "n out of range");
+    if (!d_tables || !d_bins || (n > 0 && !d_points)) return fail(WASABI_EINVAL, "NULL buffer");
+    if (!aligned(d_bins, 256)) return fail(WASABI_EINVAL, "d_bins must be 256-byte aligned");
+    if (n > 0 && !aligned(d_points, 16)) return fail(WASABI_EINVAL, "d_points must be 16-byte aligned");
+    BinLayout b = bin_layout(g, n, row0, row1);
+    if (bin_bytes < b.bytes) return fail(WASABI_ENOSPC, "bin buffer needs %zu bytes", b.bytes);
+    CK(launch_write_blob(d_bins, &b.h, sizeof b.h, stream), "write bin header");
+    const KDesc *kd = reinterpret_cast<const KDesc *>(static_cast<const char *>(d_tables) + g.th.kdesc_off);
+    CK(launch_bin(b.h, d_bins, kd, reinterpret_cast<const float4 *>(d_points), params->pitch_m, params->n_h,
+                  params->z_min_m, g.dz, g.nd, stream),
+       "bin");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables, const void *d_bins, int64_t row0,
+                               int64_t row1, float *d_psi, cudaStream_t stream) {
+    wasabi_status st = validate(params);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (!d_tables || !d_bins || (!d_psi && row1 > row0)) return fail(WASABI_EINVAL, "NULL buffer");
+    if (!aligned(d_psi, 16)) return fail(WASABI_EINVAL, "d_psi must be 16-byte aligned");
+    const int T = params->tile;
+    CK(launch_superpose_v1(d_bins, d_tables, T, T + 1, params->levels, (int)(params->n_h / T),
+                           (int)((row1 - row0) / T), row0, params->n_h, reinterpret_cast<float2 *>(d_psi), stream),
+       "superpose");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi, float *d_u, int64_t row0,
+                                int64_t row1, const wasabi_print_params *print, uint8_t *d_bits, cudaStream_t stream) {
+    wasabi_status st = validate(params);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (params->n_h % 64 || (row1 - row0) % 64) return fail(WASABI_EINVAL, "n_h and band height must be multiples of 64");
+    if (!d_psi && row1 > row0) return fail(WASABI_EINVAL, "NULL d_psi");
+    if (d_bits && !print) return fail(WASABI_EINVAL, "d_bits needs print params");
+    if (!aligned(d_psi, 16) || !aligned(d_u, 16)) return fail(WASABI_EINVAL, "fields must be 16-byte aligned");
+    double p4[4];
+    if (print) { p4[0] = print->x_r_m; p4[1] = print->y_r_m; p4[2] = print->z_r_m; p4[3] = 1.0 / params->wavelength_m; }
+    CK(launch_inverse(reinterpret_cast<const float2 *>(d_psi), reinterpret_cast<float2 *>(d_u), row1 - row0,
+                      params->n_h, row0, params->levels, print ? p4 : nullptr, params->pitch_m, d_bits, stream),
+       "inverse_wt");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_quantize(const wasabi_params *params, const wasabi_print_params *print, const float *d_u,
+                              int64_t row0, int64_t row1, uint8_t *d_bits, cudaStream_t stream) {
+    wasabi_status st = validate(params);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (!print) return fail(WASABI_EINVAL, "print params NULL");
+    if ((!d_u || !d_bits) && row1 > row0) return fail(WASABI_EINVAL, "NULL buffer");
+    if (!aligned(d_u, 16)) return fail(WASABI_EINVAL, "d_u must be 16-byte aligned");
+    double p4[4] = {print->x_r_m, print->y_r_m, print->z_r_m, 1.0 / params->wavelength_m};
+    CK(launch_quantize(reinterpret_cast<const float2 *>(d_u), row1 - row0, params->n_h, row0, p4, params->pitch_m,
+                       d_bits, stream),
+       "quantize");
+    return WASABI_OK;
+}
+
+// ---------------------------------------------------------------- whole path from host buffers
+
+namespace {
+struct WsLayout {
+    size_t tables, scratch, points, bins, field, bits, total;
+    size_t table_bytes, scratch_bytes, bin_bytes;
+};
+wasabi_status ws_layout(const wasabi_params *P, int64_t n, int64_t row0, int64_t row1, WsLayout &w) {
+    Geo g;
+    wasabi_status st = compute_geo(P, g);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(P, row0, row1)) != WASABI_OK) return st;
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(WASABI_EINVAL, "n out of range");
+    w.table_bytes = g.table_bytes;
+    w.scratch_bytes = g.scratch_bytes;
+    w.bin_bytes = bin_layout(g, n, row0, row1).bytes;
+    size_t o = 0;
+    w.tables = o; o = align_up(o + w.table_bytes, 256);
+    w.scratch = o; o = align_up(o + w.scratch_bytes, 256);
+    w.points = o; o = align_up(o + 16 * (size_t)n, 256);
+    w.bins = o; o = align_up(o + w.bin_bytes, 256);
+    w.field = o; o = align_up(o + 8 * (size_t)(row1 - row0) * (size_t)P->n_h, 256);
+    w.bits = o; o = align_up(o + (size_t)(row1 - row0) * (size_t)(P->n_h / 8), 256);
+    w.total = o;
+    return WASABI_OK;
+}
+}  // namespace
+
+wasabi_status wasabi_hologram_workspace_bytes(const wasabi_params *params, int64_t n, int64_t row0, int64_t row1,
+                                              size_t *workspace_bytes) {
+    WsLayout w;
+    wasabi_status st = ws_layout(params, n, row0, row1, w);
+    if (st != WASABI_OK) return st;
+    if (workspace_bytes) *workspace_bytes = w.total;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_print_params *print, const float *h_points,
+                                   int64_t n, int64_t row0, int64_t row1, void *d_workspace, size_t workspace_bytes,
+                                   uint8_t *h_bits, float *h_u, cudaStream_t stream) {
+    WsLayout w;
+    wasabi_status st = ws_layout(params, n, row0, row1, w);
+    if (st != WASABI_OK) return st;
+    if (!print) return fail(WASABI_EINVAL, "print params NULL");
+    if (!d_workspace || (n > 0 && !h_points)) return fail(WASABI_EINVAL, "NULL buffer");
+    if (!aligned(d_workspace, 256)) return fail(WASABI_EINVAL, "workspace must be 256-byte aligned");
+    if (workspace_bytes < w.total) return fail(WASABI_ENOSPC, "workspace needs %zu bytes", w.total);
+    char *ws = static_cast<char *>(d_workspace);
+    float *d_pts = reinterpret_cast<float *>(ws + w.points);
+    float *d_field = reinterpret_cast<float *>(ws + w.field);
+    uint8_t *d_bits = reinterpret_cast<uint8_t *>(ws + w.bits);
+    if (n > 0) CK(cudaMemcpyAsync(d_pts, h_points, 16 * (size_t)n, cudaMemcpyHostToDevice, stream), "H2D points");
+    if ((st = wasabi_build_psf_tables(params, ws + w.tables, w.table_bytes, ws + w.scratch, w.scratch_bytes, stream)))
+        return st;
+    if ((st = wasabi_bin_points(params, ws + w.tables, d_pts, n, row0, row1, ws + w.bins, w.bin_bytes, stream)))
+        return st;
+    if ((st = wasabi_superpose(params, ws + w.tables, ws + w.bins, row0, row1, d_field, stream))) return st;
+    if ((st = wasabi_inverse_wt(params, d_field, d_field, row0, row1, print, d_bits, stream))) return st;
+    const size_t nbits = (size_t)(row1 - row0) * (size_t)(params->n_h / 8);
+    if (h_bits && nbits) CK(cudaMemcpyAsync(h_bits, d_bits, nbits, cudaMemcpyDeviceToHost, stream), "D2H bits");
+    if (h_u && row1 > row0)
+        CK(cudaMemcpyAsync(h_u, d_field, 8 * (size_t)(row1 - row0) * (size_t)params->n_h, cudaMemcpyDeviceToHost,
+                           stream),
+           "D2H u");
+    return WASABI_OK;
+}
+
+// ---------------------------------------------------------------- diagnostics
+
+wasabi_status wasabi_tables_check(const wasabi_params *params, const void *d_tables) {
+    wasabi_status st = validate(params);
+    if (st != WASABI_OK) return st;
+    TableHeader h;
+    CK(cudaMemcpy(&h, d_tables, sizeof h, cudaMemcpyDeviceToHost), "read table header");
+    if (h.magic != kTableMagic) return fail(WASABI_ESTATE, "not a WASABI table buffer");
+    if (h.param_hash != param_hash(*params)) return fail(WASABI_ESTATE, "table buffer was built with other params");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_export_table(const wasabi_params *params, const void *d_tables, int32_t depth, int32_t *h_level,
+                                  int32_t *h_dx, int32_t *h_dy, float *h_val, int64_t cap, int64_t *n_out) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if ((st = wasabi_tables_check(params, d_tables)) != WASABI_OK) return st;
+    if (depth < 0 || depth >= g.nd) return fail(WASABI_EINVAL, "depth out of range");
+    const char *tb = static_cast<const char *>(d_tables);
+    const KDesc K = g.kd[depth];
+    const DDesc D = g.dd[depth];
+    std::vector<int32_t> ptr(D.n_groups + 1);
+    CK(cudaMemcpy(ptr.data(), tb + g.th.ptr_off + 4 * (size_t)D.group_base, 4 * ptr.size(), cudaMemcpyDeviceToHost),
+       "read ptr");
+    const int64_t e0 = ptr[0], e1 = ptr[D.n_groups];
+    const int64_t n = e1 - e0;
+    if (n_out) *n_out = n;
+    if (n != D.n_r) return fail(WASABI_ESTATE, "depth %d holds %lld entries, expected N_r = %lld", depth,
+                                (long long)n, (long long)D.n_r);
+    if (cap < n) return fail(WASABI_ENOSPC, "need capacity %lld", (long long)n);
+    std::vector<uint32_t> pos(n);
+    std::vector<float> val(2 * n);
+    if (n) {
+        CK(cudaMemcpy(pos.data(), tb + g.th.pos_off + 4 * (size_t)e0, 4 * (size_t)n, cudaMemcpyDeviceToHost), "read pos");
+        CK(cudaMemcpy(val.data(), tb + g.th.val_off + 8 * (size_t)e0, 8 * (size_t)n, cudaMemcpyDeviceToHost), "read val");
+    }
+    struct Rec { int32_t l, Y, X; int64_t i; };
+    std::vector<Rec> rec;
+    rec.reserve(n);
+    const int64_t H = K.H;
+    for (int l = 1; l <= g.L; l++) {
+        const int64_t nb = (2 * H) >> l, hb = band_blocks(g.T, l), nbands = (nb + hb - 1) / hb;
+        const int64_t gl = K.ptr_base[l - 1] - D.group_base;
+        for (int64_t band = 0; band < nbands; band++)
+            for (int64_t Xb = 0; Xb < nb; Xb++) {
+                const int64_t gi = gl + band * (nb + 1) + Xb;
+                for (int64_t i = ptr[gi]; i < ptr[gi + 1]; i++) {
+                    const uint32_t p = pos[i - e0];
+                    const int64_t u = p >> 16, w = p & 0xffff, v = w - u * g.S;
+                    const int64_t Xb2 = v >> 1, sbx = v & 1, Yb = band * hb + (u >> 1), sby = u & 1;
+                    if (Xb2 != Xb) return fail(WASABI_ESTATE, "corrupt position record");
+                    rec.push_back(Rec{l, (int32_t)((Yb << l) + sby * (1 << (l - 1))),
+                                      (int32_t)((Xb2 << l) + sbx * (1 << (l - 1))), i - e0});
+                }
+            }
+    }
+    std::sort(rec.begin(), rec.end(), [](const Rec &a, const Rec &b) {
+        if (a.l != b.l) return a.l < b.l;
+        if (a.Y != b.Y) return a.Y < b.Y;
+        return a.X < b.X;
+    });
+    for (int64_t k = 0; k < n; k++) {
+        if (h_level) h_level[k] = rec[k].l;
+        if (h_dx) h_dx[k] = (int32_t)(rec[k].X - H);
+        if (h_dy) h_dy[k] = (int32_t)(rec[k].Y - H);
+        if (h_val) { h_val[2 * k] = val[2 * rec[k].i]; h_val[2 * k + 1] = val[2 * rec[k].i + 1]; }
+    }
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_bins_stats(const void *d_bins, int64_t out[8]) {
+    if (!d_bins || !out) return fail(WASABI_EINVAL, "NULL argument");
+    BinHeader h;
+    CK(cudaMemcpy(&h, d_bins, sizeof h, cudaMemcpyDeviceToHost), "read bin header");
+    if (h.magic != kBinMagic) return fail(WASABI_ESTATE, "not a WASABI bin buffer");
+    out[0] = (int64_t)h.n_valid; out[1] = (int64_t)h.n_skipped; out[2] = (int64_t)h.total_entries;
+    out[3] = h.capacity; out[4] = h.row0; out[5] = h.row1; out[6] = h.n_tiles; out[7] = (int64_t)h.status;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_export_bins(const wasabi_params *params, const void *d_bins, int64_t *h_tile_ptr,
+                                 int32_t *h_point_idx, int64_t cap, int64_t *n_out) {
+    wasabi_status st = validate(params);
+    if (st != WASABI_OK) return st;
+    BinHeader h;
+    CK(cudaMemcpy(&h, d_bins, sizeof h, cudaMemcpyDeviceToHost), "read bin header");
+    if (h.magic != kBinMagic) return fail(WASABI_ESTATE, "not a WASABI bin buffer");
+    if (h.param_hash != param_hash(*params)) return fail(WASABI_ESTATE, "bins were built with other params");
+    if (h.status) return fail(WASABI_ESTATE, "bin buffer overflowed (status %llu)", (unsigned long long)h.status);
+    const char *bb = static_cast<const char *>(d_bins);
+    std::vector<unsigned long long> ptr(h.n_tiles + 1);
+    CK(cudaMemcpy(ptr.data(), bb + h.ptr_off, 8 * ptr.size(), cudaMemcpyDeviceToHost), "read bin ptr");
+    const int64_t n = (int64_t)ptr[h.n_tiles];
+    if (n_out) *n_out = n;
+    if (h_tile_ptr)
+        for (int64_t i = 0; i <= h.n_tiles; i++) h_tile_ptr[i] = (int64_t)ptr[i];
+    if (h_point_idx) {
+        if (cap < n) return fail(WASABI_ENOSPC, "need capacity %lld", (long long)n);
+        if (n) CK(cudaMemcpy(h_point_idx, bb + h.idx_off, 4 * (size_t)n, cudaMemcpyDeviceToHost), "read bin idx");
+    }
+    return WASABI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+"""Pipeline: owns the device buffers of one band and runs steps 1-4 on one CUDA stream.
+
+Marshalling and buffer management only (torch allocates; the C ABI computes).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+from . import (Params, PrintParams, bin_points, bin_points_bytes, build_psf_tables, inverse_wt,
+               psf_tables_bytes, quantize, superpose)
+
+
+class Pipeline:
+    """Device buffers for band [row0, row1) of a hologram with params `p` and up to n_max points.
+
+    run(points) executes: build tables (step 1) -> bin (2a) -> superpose (2b) -> inverse (3),
+    fused with quantise (4) when `bits` is requested.  `u` is written in place over psi.
+    """
+
+    def __init__(self, p: Params, n_max: int, row0: int = 0, row1: Optional[int] = None, device=None,
+                 want_u: bool = True, want_bits: bool = True, print_params: Optional[PrintParams] = None,
+                 stream=None):
+        import torch
+        self.torch = torch
+        self.p = p
+        self.row0 = row0
+        self.row1 = p.n_h if row1 is None else row1
+        self.device = torch.device(device if device is not None else "cuda")
+        self.n_max = n_max
+        self.print_params = print_params if print_params is not None else PrintParams()
+        tb, sb = psf_tables_bytes(p)
+        self.tables = torch.empty(tb, dtype=torch.uint8, device=self.device)
+        self.scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        self.bins = torch.empty(bin_points_bytes(p, n_max, self.row0, self.row1), dtype=torch.uint8,
+                                device=self.device)
+        rows = self.row1 - self.row0
+        self.field = torch.empty((rows, p.n_h, 2), dtype=torch.float32, device=self.device)
+        self.bits = torch.empty((rows, p.n_h // 8), dtype=torch.uint8, device=self.device) if want_bits else None
+        self.want_u = want_u
+        self.stream = stream
+        self.tables_built = False
+
+    def nbytes(self) -> int:
+        t = self.tables.numel() + self.scratch.numel() + self.bins.numel() + self.field.numel() * 4
+        return t + (self.bits.numel() if self.bits is not None else 0)
+
+    # individual steps (all asynchronous on the stream)
+    def build_tables(self):
+        build_psf_tables(self.p, self.tables, self.scratch, self.stream)
+        self.tables_built = True
+
+    def bin(self, points):
+        bin_points(self.p, self.tables, points, self.row0, self.row1, self.bins, self.stream)
+
+    def superpose(self):
+        superpose(self.p, self.tables, self.bins, self.row0, self.row1, self.field, self.stream)
+
+    def inverse(self, fuse_bits: bool = True):
+        bits = self.bits if (fuse_bits and self.bits is not None) else None
+        u = self.field if self.want_u else None
+        inverse_wt(self.p, self.field, u, self.row0, self.row1, self.print_params, bits, self.stream)
+
+    def quantize(self):
+        quantize(self.p, self.print_params, self.field, self.row0, self.row1, self.bits, self.stream)
+
+    def run(self, points, build_tables: bool = True):
+        if build_tables or not self.tables_built:
+            self.build_tables()
+        self.bin(points)
+        self.superpose()
+        self.inverse()
+        return self.field, self.bits

@@ -1,0 +1,308 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Bars (north_star): top-k index lists and bins bit-exact; psi and u within 1e-5
+relative L2 (fp32 GPU vs fp64 oracle); print bits identical except on pixels inside the threshold
+band (R-A16, helpers.bits_mismatch_outside_band)."""
+import numpy as np
+import pytest
+
+from helpers import (CONFIGS, REF, bits_mismatch_outside_band, field_np, gpu_params, make_points, orc_params,
+                     rel_l2)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def W():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1708_04233_b200 as W
+    return W
+
+
+def _tables(W, p):
+    import torch
+    tb, sb = W.psf_tables_bytes(p)
+    t = torch.empty(tb, dtype=torch.uint8, device="cuda")
+    s = torch.empty(sb, dtype=torch.uint8, device="cuda")
+    W.build_psf_tables(p, t, s)
+    torch.cuda.synchronize()
+    W.tables_check(p, t)
+    return t
+
+
+def _compare_depth(W, orc, p, P, t, d):
+    lv, dx, dy, val = W.export_table(p, t, d)
+    n_r = W.depth_geometry(p, d)["n_r"]
+    olv, odx, ody, oval = orc.select(P, d, n_r)
+    assert len(lv) == n_r
+    assert np.array_equal(lv, olv) and np.array_equal(dx, odx) and np.array_equal(dy, ody), f"depth {d}"
+    scale = np.max(np.abs(oval))
+    assert np.max(np.abs(val - oval)) <= 1e-6 * scale + 1e-7, f"depth {d} values"
+
+
+# ---------------------------------------------------------------- step 1: tables (bit-exact indices)
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", dict(retention=0.01)), ("C2", dict(retention=0.05)),
+                                     ("C2", {}), ("C3", {}), ("C5", dict(retention=1.0)),
+                                     ("C1", dict(levels=1)), ("C1", dict(levels=6, tile=128))])
+def test_tables_bitexact(W, orc, name, kw):
+    cfg = CONFIGS[name].replace(**{k: v for k, v in kw.items() if k in ("retention", "levels", "tile")})
+    p = gpu_params(cfg)
+    P = orc_params(orc, cfg)
+    t = _tables(W, p)
+    depths = range(cfg.n_depth) if cfg.n_depth <= 16 else sorted({0, 1, cfg.n_depth // 3, cfg.n_depth // 2,
+                                                                   cfg.n_depth - 2, cfg.n_depth - 1})
+    for d in depths:
+        _compare_depth(W, orc, p, P, t, d)
+
+
+def test_tables_bitexact_c4_sample(W, orc):
+    cfg = CONFIGS["C4"]
+    p = gpu_params(cfg)
+    P = orc_params(orc, cfg)
+    t = _tables(W, p)
+    for d in (0, 31, 63, 64, 100, 127):   # |z| = 2 mm (largest table, 1408^2) ... 0.016 mm
+        _compare_depth(W, orc, p, P, t, d)
+
+
+# ---------------------------------------------------------------- step 2a: bins (bit-exact)
+@pytest.mark.parametrize("name,n,row0,row1", [("C1", None, 0, 512), ("C1", None, 128, 320), ("C2", None, 0, 2048),
+                                              ("C2", 3000, 1024, 1536), ("C3", 20000, 0, 8192)])
+def test_bins_bitexact(W, orc, name, n, row0, row1):
+    import torch
+    cfg = CONFIGS[name]
+    pts = make_points(cfg, n=n)
+    pts[::97, 3] = -1.0           # skipped points
+    p = gpu_params(cfg)
+    P = orc_params(orc, cfg)
+    t = _tables(W, p)
+    bins = torch.empty(W.bin_points_bytes(p, len(pts), row0, row1), dtype=torch.uint8, device="cuda")
+    W.bin_points(p, t, torch.from_numpy(pts).cuda(), row0, row1, bins)
+    torch.cuda.synchronize()
+    st = W.bins_stats(bins)
+    assert st["status"] == 0 and st["n_skipped"] == len(pts[::97])
+    ptr_g, idx_g = W.export_bins(p, bins)
+    ptr_o, idx_o = orc.bins(P, p.tile, pts, row0, row1)
+    assert np.array_equal(ptr_g, ptr_o)
+    assert np.array_equal(idx_g, idx_o)
+
+
+# ---------------------------------------------------------------- steps 2b-4: fields and bits
+def _gpu_run(W, cfg, pts, row0, row1, **kw):
+    import torch
+    p = gpu_params(cfg, **kw)
+    pl = W.Pipeline(p, max(1, len(pts)), row0, row1)
+    d_pts = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+    pl.build_tables()
+    pl.bin(d_pts)
+    pl.superpose()
+    psi = field_np(pl.field)
+    pl.inverse()
+    torch.cuda.synchronize()
+    return pl, psi, field_np(pl.field), pl.bits.cpu().numpy()
+
+
+def _check_fields(orc, cfg, pts, row0, row1, pl, psi_g, u_g, bits_g, x0=0, w=None, **kw):
+    P = orc_params(orc, cfg, **kw)
+    w = cfg.n_h if w is None else w
+    lut = orc.Lut(P)
+    u_o, psi_o, _ = lut.hologram_window(pts, x0, row0, w, row1 - row0)
+    psi_gw = psi_g[:, x0:x0 + w]
+    u_gw = u_g[:, x0:x0 + w]
+    e_psi, e_u = rel_l2(psi_gw, psi_o), rel_l2(u_gw, u_o)
+    assert e_psi <= 1e-5, e_psi
+    assert e_u <= 1e-5, e_u
+    bits_o, I_o = orc.quantize(P, REF, u_o, x0, row0)
+    bad, nd, nband = bits_mismatch_outside_band(bits_g[:, x0 // 8:(x0 + w) // 8], bits_o, I_o,
+                                                np.abs(u_gw - u_o), np.abs(u_o))
+    assert bad == 0, f"{bad} print bits differ outside the threshold band ({nd} total flips)"
+    return e_psi, e_u
+
+
+@pytest.mark.parametrize("name,n,row0,row1", [("C1", None, 0, 512), ("C1", None, 192, 448),
+                                              ("C2", None, 0, 2048), ("C2", 4000, 640, 1152)])
+def test_field_parity(W, orc, name, n, row0, row1):
+    cfg = CONFIGS[name]
+    pts = make_points(cfg, n=n)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, row0, row1)
+    _check_fields(orc, cfg, pts, row0, row1, pl, psi_g, u_g, bits_g)
+
+
+@pytest.mark.parametrize("r", [0.01, 0.05])
+def test_field_parity_c2_retentions(W, orc, r):
+    cfg = CONFIGS["C2"].replace(retention=r)
+    pts = make_points(cfg, n=5000)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 0, 2048)
+    _check_fields(orc, cfg, pts, 0, 2048, pl, psi_g, u_g, bits_g)
+
+
+def test_field_parity_c3_band(W, orc):
+    """C3 (8192^2, 532 nm, RGB-D surface, L=5, r=5%): full GPU band of 512 rows vs oracle."""
+    cfg = CONFIGS["C3"]
+    pts = make_points(cfg)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 4096, 4608)
+    _check_fields(orc, cfg, pts, 4096, 4608, pl, psi_g, u_g, bits_g, x0=2048, w=2048)
+
+
+@pytest.mark.parametrize("kw", [dict(tile=128), dict(levels=1), dict(levels=6, tile=128),
+                                dict(retention=1.0)])
+def test_field_parity_variants(W, orc, kw):
+    cfg = CONFIGS["C1"].replace(**kw)
+    pts = make_points(cfg, n=600)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 0, cfg.n_h)
+    _check_fields(orc, cfg, pts, 0, cfg.n_h, pl, psi_g, u_g, bits_g)
+
+
+def test_aligned_keep_all_equals_direct_sum(W, orc):
+    """V3 on the GPU: r=100%, 2^L-aligned points on levels -> u equals the D2 direct sum."""
+    cfg = CONFIGS["C1"].replace(retention=1.0, aligned=True, kind="levels")
+    pts = make_points(cfg, n=200)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 0, cfg.n_h)
+    P = orc_params(orc, cfg)
+    d2 = orc.direct_d2(P, pts.astype(np.float64), 0, 0, cfg.n_h, cfg.n_h)
+    assert rel_l2(u_g, d2) <= 1e-5
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_and_invalid_points(W, orc):
+    cfg = CONFIGS["C1"]
+    for pts in (np.zeros((0, 4), np.float32),
+                np.array([[0, 0, 0.2e-3, 0.0], [np.nan, 0, 0.2e-3, 1], [0, 0, 5e-3, 1]], np.float32),
+                np.array([[0.9e-3, 0.9e-3, 0.2e-3, 1.0]], np.float32)):     # PSF far outside
+        pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 0, cfg.n_h)
+        assert np.all(psi_g == 0) and np.all(u_g == 0)
+
+
+def test_points_outside_aperture_contribute(W, orc):
+    """A point outside the hologram whose PSF overlaps it contributes (R-A12: partial bins)."""
+    cfg = CONFIGS["C1"]
+    pts = np.array([[-0.27e-3, 0.1e-3, 0.4e-3, 1.0], [0.26e-3, -0.3e-3, 0.35e-3, 0.5]], np.float32)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 0, cfg.n_h)
+    assert np.any(u_g != 0)
+    _check_fields(orc, cfg, pts, 0, cfg.n_h, pl, psi_g, u_g, bits_g)
+
+
+def test_band_split_is_bitwise_identical(W):
+    """Row bands (the multi-GPU split) concatenate to the single-band result
+    bit for bit: no halo, fixed per-pixel accumulation order."""
+    cfg = CONFIGS["C2"]
+    pts = make_points(cfg, n=4000)
+    _, _, u_full, b_full = _gpu_run(W, cfg, pts, 0, 2048)
+    parts_u, parts_b = [], []
+    for b in range(4):
+        _, _, u, bb = _gpu_run(W, cfg, pts, b * 512, (b + 1) * 512)
+        parts_u.append(u)
+        parts_b.append(bb)
+    assert np.array_equal(np.concatenate(parts_u), u_full)
+    assert np.array_equal(np.concatenate(parts_b), b_full)
+
+
+def test_deterministic_repeat(W):
+    cfg = CONFIGS["C2"]
+    pts = make_points(cfg, n=3000)
+    _, p1, u1, b1 = _gpu_run(W, cfg, pts, 0, 2048)
+    _, p2, u2, b2 = _gpu_run(W, cfg, pts, 0, 2048)
+    assert np.array_equal(p1, p2) and np.array_equal(u1, u2) and np.array_equal(b1, b2)
+
+
+# ---------------------------------------------------------------- steps 3 and 4 standalone
+@pytest.mark.parametrize("L", [1, 3, 6])
+def test_inverse_standalone(W, orc, L):
+    import torch
+    cfg = CONFIGS["C1"].replace(levels=L, tile=64)
+    p = gpu_params(cfg)
+    rng = np.random.default_rng(L)
+    psi = (rng.standard_normal((128, 512)) + 1j * rng.standard_normal((128, 512))).astype(np.complex64)
+    d = torch.from_numpy(np.stack([psi.real, psi.imag], -1).astype(np.float32)).cuda()
+    u = torch.empty_like(d)
+    W.inverse_wt(p, d, u, 64, 192)
+    torch.cuda.synchronize()
+    u_o = orc.haar_inv(psi.astype(np.complex128), L)
+    assert rel_l2(field_np(u), u_o) <= 1e-6
+
+
+def test_quantize_standalone_same_input(W, orc):
+    """Step 4 alone on the same u: bits identical except |I| <= 1e-6 rms(I) (the decision is taken
+    on identical inputs; only the fp64 phase reduction / fp32 sincos differ)."""
+    import torch
+    cfg = CONFIGS["C2"]
+    p = gpu_params(cfg)
+    rng = np.random.default_rng(5)
+    u = (rng.standard_normal((256, 2048)) + 1j * rng.standard_normal((256, 2048))).astype(np.complex64)
+    d = torch.from_numpy(np.stack([u.real, u.imag], -1)).cuda()
+    bits = torch.empty((256, 256), dtype=torch.uint8, device="cuda")
+    W.quantize(p, W.PrintParams(*REF), d, 512, 768, bits)
+    torch.cuda.synchronize()
+    P = orc_params(orc, cfg)
+    bits_o, I_o = orc.quantize(P, REF, u.astype(np.complex128), 0, 512)
+    g = np.unpackbits(bits.cpu().numpy(), axis=1, bitorder="big").astype(bool)
+    o = np.unpackbits(bits_o, axis=1, bitorder="big").astype(bool)
+    rms = np.sqrt(np.mean(I_o ** 2))
+    assert np.sum((g != o) & (np.abs(I_o) > 1e-6 * rms)) == 0
+
+
+def test_fused_equals_standalone_quantize(W):
+    import torch
+    cfg = CONFIGS["C1"]
+    pts = make_points(cfg)
+    pl, _, u_g, bits_fused = _gpu_run(W, cfg, pts, 0, 512)
+    bits = torch.empty_like(pl.bits)
+    W.quantize(pl.p, pl.print_params, pl.field, 0, 512, bits)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits.cpu().numpy(), bits_fused)
+
+
+# ---------------------------------------------------------------- whole path from host buffers
+def test_hologram_host_equals_device_path(W):
+    import torch
+    cfg = CONFIGS["C2"]
+    pts = make_points(cfg, n=5000)
+    p = gpu_params(cfg)
+    ws = torch.empty(W.hologram_workspace_bytes(p, len(pts), 512, 1024), dtype=torch.uint8, device="cuda")
+    h_pts = torch.from_numpy(pts).pin_memory()
+    h_bits = torch.empty((512, 256), dtype=torch.uint8).pin_memory()
+    h_u = torch.empty((512, 2048, 2), dtype=torch.float32).pin_memory()
+    W.hologram_host(p, W.PrintParams(*REF), h_pts, 512, 1024, ws, h_bits, h_u)
+    torch.cuda.synchronize()
+    _, _, u_d, b_d = _gpu_run(W, cfg, pts, 512, 1024)
+    assert np.array_equal(h_bits.numpy(), b_d)
+    assert np.array_equal(field_np(h_u), u_d)
+
+
+# ---------------------------------------------------------------- full-size C4 (sampled outputs)
+def test_c4_full_size_sampled(W, orc):
+    """BASELINE configs[3] at full size (65,536^2, 2e6 points, 128 levels, L=6, r=5%) in the bench's
+    launch configuration (one GPU, all rows); 6 sampled 64x64 blocks recomputed by the oracle one by
+    one (a block's u depends only on its own psi coefficients)."""
+    import torch
+    cfg = CONFIGS["C4"]
+    pts = make_points(cfg)
+    p = gpu_params(cfg)
+    pl = W.Pipeline(p, len(pts), 0, p.n_h)
+    pl.run(torch.from_numpy(pts).cuda())
+    torch.cuda.synchronize()
+    st = W.bins_stats(pl.bins)
+    assert st["status"] == 0 and st["n_valid"] == len(pts)
+    P = orc_params(orc, cfg)
+    lut = orc.Lut(P)
+    rng = np.random.default_rng(44)
+    B = 64
+    for _ in range(6):
+        X0 = int(rng.integers(0, p.n_h // B)) * B
+        Y0 = int(rng.integers(0, p.n_h // B)) * B
+        u_o, psi_o, _ = lut.hologram_window(pts, X0, Y0, B, B)
+        u_g = field_np(pl.field[Y0:Y0 + B, X0:X0 + B])
+        assert rel_l2(u_g, u_o) <= 1e-5
+        bits_o, I_o = orc.quantize(P, REF, u_o, X0, Y0)
+        bad, _, _ = bits_mismatch_outside_band(pl.bits[Y0:Y0 + B, X0 // 8:(X0 + B) // 8].cpu().numpy(), bits_o, I_o,
+                                               np.abs(u_g - u_o), np.abs(u_o))
+        assert bad == 0
+    # sampled bins (single tiles) vs the oracle's definition, bit-exact
+    ptr_g, idx_g = W.export_bins(p, pl.bins)
+    T = p.tile
+    tiles_x = p.n_h // T
+    for t in rng.integers(0, len(ptr_g) - 1, 8):
+        X0, Y0 = int(t % tiles_x) * T, int(t // tiles_x) * T
+        assert np.array_equal(idx_g[ptr_g[t]:ptr_g[t + 1]], orc.bin_tile(P, T, pts, X0, Y0))
