@@ -1,0 +1,36 @@
+"""Profiling driver: C4-density workload restricted to one row band, runs each step once
+(plus `--reps` superpose repeats) so ncu can capture single kernels quickly."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1708_04233_b200 as W  # noqa: E402
+from inputs import CONFIGS, make_points  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C4")
+ap.add_argument("--row0", type=int, default=32768)
+ap.add_argument("--rows", type=int, default=512)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--tile", type=int, default=None)
+a = ap.parse_args()
+cfg = CONFIGS[a.config]
+if a.tile:
+    cfg = cfg.replace(tile=a.tile)
+p = W.Params.from_config(cfg)
+pts = make_points(cfg)
+pl = W.Pipeline(p, len(pts), a.row0, a.row0 + a.rows)
+d = torch.from_numpy(pts).cuda()
+pl.run(d)
+torch.cuda.synchronize()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ev[0].record()
+for _ in range(a.reps):
+    pl.superpose()
+ev[1].record()
+torch.cuda.synchronize()
+st = W.bins_stats(pl.bins)
+print(f"superpose {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
