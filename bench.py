@@ -27,7 +27,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from inputs import CONFIGS, make_points  # noqa: E402
-from inputs.generators import band_rows  # noqa: E402
 
 METRIC = "object points/s and hologram Gpixel/s (WASABI superpose+inverse WT), % of HBM roofline"
 UNIT = "Gpixel/s"
@@ -185,7 +184,8 @@ def run_ours(args, cfg):
         return float(t.item())
 
     p = W.Params.from_config(cfg)
-    row0, row1 = band_rows(cfg.n_h, world, rank, p.tile)
+    from paper_1708_04233_b200.distributed import band_of, checksums, gather_checksums
+    row0, row1 = band_of(rank, world, cfg.n_h, p.tile)
     pts = make_points(cfg)
     n = len(pts)
     d_pts = torch.from_numpy(pts).to(dev)
@@ -232,12 +232,10 @@ def run_ours(args, cfg):
     points_per_s = n / (ms_per_step * 1e-3)
 
     # checksum assembly after the timed region (the only collective: NCCL all_gather)
-    u_energy = float((pl.field.double() ** 2).sum().item()) if cfg.n_h <= 16384 else None
-    pop = int(pl.bits.to(torch.int32).bitwise_and(0xFF).sum().item()) if pl.bits is not None else 0
+    cs = checksums(pl.field, pl.bits)
     if world > 1:
-        mine = torch.tensor([float(pop)], dtype=torch.float64, device=dev)
-        allv = [torch.zeros_like(mine) for _ in range(world)]
-        dist.all_gather(allv, mine)
+        cs = gather_checksums(cs).sum(dim=0)
+    cs = cs.tolist()
 
     # roofline of the dominant kernel (algorithmic bytes per launch / event-timed duration)
     peak, peak_src = _peaks()
@@ -301,7 +299,7 @@ def run_ours(args, cfg):
                           "l2": f"inputs larger than L2 (psi/u {8 * rows * cfg.n_h / 1e9:.1f} GB per GPU per step)"},
                "points_per_s": points_per_s, "stage_ms": stage_ms, "bin_entries": st["entries"],
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-               "clocks": ck, "checksum": {"bits_bytes_sum": pop, "u_energy": u_energy},
+               "clocks": ck, "checksum": {"u_energy": cs[0], "u_re_sum": cs[1], "u_im_sum": cs[2], "bits_set": cs[3]},
                "paper_context": {"wasabi_s_65536sq_95949pts_cpu": 354, "nlut_s": 10533,
                                  "cite": "PAPER.md:166 (Xeon E5 v3; different point count and wavelet)"}}
         print(json.dumps(out), flush=True)

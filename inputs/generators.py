@@ -124,11 +124,3 @@ def make_points(cfg: Config, n: Optional[int] = None, seed: Optional[int] = None
     pts[:, 2] = z
     pts[:, 3] = a
     return pts
-
-
-def band_rows(n_h: int, n_bands: int, band: int, align: int):
-    """Equal row bands [row0, row1) whose edges are multiples of `align` (tile and 2^L)."""
-    if n_h % (n_bands * align) != 0:
-        raise ValueError(f"n_h={n_h} not divisible into {n_bands} bands aligned to {align}")
-    h = n_h // n_bands
-    return band * h, (band + 1) * h
