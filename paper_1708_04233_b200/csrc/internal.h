@@ -9,7 +9,14 @@ namespace wasabi {
 constexpr uint64_t kTableMagic = 0x3142545942415357ull;  // "WSABYTB1"
 constexpr uint64_t kBinMagic = 0x314e494249425357ull;    // "WSBIBIN1"
 constexpr int kMaxLevels = 6;
-constexpr int kMaxTableSide = 16384;  // 2H limit: packed positions use 13/14-bit block indices
+constexpr int kMaxTableSide = 16384;  // 2H limit: entry positions are packed as 14-bit X and Y
+
+// LUT entry (16 bytes, 16-byte aligned so that any range of entries is a legal TMA bulk copy):
+//   x = X | Y << 14 | level << 28   (table coordinates of the coefficient, level 1..L; LL is level L)
+//   y, z = value (re, im) as float bits, w = 0
+__host__ __device__ inline uint32_t pack_entry_pos(int X, int Y, int level) {
+    return (uint32_t)X | ((uint32_t)Y << 14) | ((uint32_t)level << 28);
+}
 
 // Compact per-depth data read by the hot kernels (32 bytes).
 struct KDesc {
@@ -38,7 +45,8 @@ struct TableHeader {
     int64_t total_entries;             // sum N_r,d
     int64_t total_ptrs;                // int32 pointer slots
     int64_t total_ctas;                // K1 grid
-    int64_t kdesc_off, ddesc_off, val_off, pos_off, ptr_off, ctabase_off;  // byte offsets
+    int64_t kdesc_off, ddesc_off, ent_off, ptr_off, ctabase_off;  // byte offsets
+    int64_t pad0;
     int64_t table_bytes;
     int64_t pad[3];
 };

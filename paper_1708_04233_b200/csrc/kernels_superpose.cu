@@ -10,11 +10,12 @@
 // ("slot"; <= 32 slots per point).  Per batch of kPB points:
 //   ranges   lane s computes slot s of each point (two independent points per step for ILP),
 //            compacts the non-empty ranges and scans their counts -> 8-byte range records
-//            (entry offset, base | shift << 23) in shared memory;
+//            (entry offset, smem base of the point's level) in shared memory;
 //   stream   the warp streams the flattened entries 32 at a time (a chunk never mixes points, so
 //            all targets of a chunk are distinct: no atomics, no races).  The current point's range
 //            prefixes live in registers (lane r holds range r); lane -> range uses one REDUX.OR
 //            marker + two POPCs; a kD-deep register ring prefetches the entry loads.
+// LUT entries are 16-byte records (X | Y << 14 | level << 28, re, im): target = Y*S + X + base.
 // Rows outside the tile (band rounding) are rejected by one unsigned compare of the smem address
 // (X ranges are exact).  psi is written once, coalesced.  Per-pixel accumulation order is fixed
 // (point order): bitwise deterministic and independent of the band split.
@@ -34,7 +35,7 @@ struct SupArgs {
 constexpr int kPB = 8;                 // points per range batch
 constexpr int kD = 8;                  // prefetch depth (chunks)
 constexpr int kEmpty = 0x3fffffff;
-constexpr int kBadBase = 0x3fffff;     // base of padding lanes: address always >= T*S
+constexpr int kBadBase = 0x3fffffff;   // base of padding lanes: address always >= T*S
 
 __device__ __forceinline__ float2 lds2(uint32_t a) {
     float2 v;
@@ -71,8 +72,7 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
     const TableHeader *th = reinterpret_cast<const TableHeader *>(tb);
     const KDesc *__restrict__ kd = reinterpret_cast<const KDesc *>(tb + th->kdesc_off);
     const int32_t *__restrict__ tptr = reinterpret_cast<const int32_t *>(tb + th->ptr_off);
-    const float2 *__restrict__ tval = reinterpret_cast<const float2 *>(tb + th->val_off);
-    const uint32_t *__restrict__ tpos = reinterpret_cast<const uint32_t *>(tb + th->pos_off);
+    const uint4 *__restrict__ tent = reinterpret_cast<const uint4 *>(tb + th->ent_off);
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cls = wid & 1, half = wid >> 1;
@@ -117,7 +117,6 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
     const int my_tx = tile_x0 >> l_;
     const int my_ty = sub_y0 >> l_;
     const int my_Wy = (((sub_y0 + Th - 1) >> l_) + 1) - my_ty;
-    const int bs_shift = (l_ - 1) << 23;
     const unsigned seg_bits = SEGW == 32 ? 0xffffffffu : ((1u << SEGW) - 1u);
     const unsigned seg_lt = ((1u << slot) - 1u) << (seg * SEGW);
     __syncthreads();
@@ -158,8 +157,7 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
                 const int row = pbs[h] + band * (nb + 1);
                 beg[h] = 0; end[h] = 0;
                 if (ok) { beg[h] = __ldg(tptr + row + xb0c); end[h] = __ldg(tptr + row + xb1c); }
-                bse[h] = ((((band * my_hb) << l_) - H[h] + (sy << l_) - tile_y0) * S + ((sx << l_) - H[h] - tile_x0)) &
-                         0x7fffff;
+                bse[h] = ((sy << l_) - H[h] - tile_y0) * S + ((sx << l_) - H[h] - tile_x0);
             }
 #pragma unroll
             for (int h = 0; h < kH; h++) {
@@ -185,7 +183,7 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
                 if (mine) {
                     if (c > 0) {
                         const int p = __popc(bal & seg_lt);
-                        rec_s[idx][p] = make_int2(beg[h] - excl, bse[h] | bs_shift);
+                        rec_s[idx][p] = make_int2(beg[h] - excl, bse[h]);
                         ex_s[idx][p] = excl;
                     }
                     if (slot >= __popc(mine)) ex_s[idx][slot] = kEmpty;
@@ -222,10 +220,9 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
             const int e = cp + lane;                                                        \
             const int2 d = rec_s[kp][rr & (SEGW - 1)];                                      \
             if (e < totp) {                                                                 \
-                const int i = e + d.x;                                                      \
-                rw[s] = __ldg(tpos + i);                                                    \
-                const float2 v = __ldg(tval + i);                                           \
-                rx[s] = v.x; ry[s] = v.y; rb[s] = d.y; ra[s] = ap;                          \
+                const uint4 en = __ldg(tent + e + d.x);                                     \
+                rw[s] = en.x; rx[s] = __uint_as_float(en.y); ry[s] = __uint_as_float(en.z); \
+                rb[s] = d.y; ra[s] = ap;                                                    \
             }                                                                               \
             cp += 32;                                                                       \
             if (cp >= totp) {                                                               \
@@ -238,8 +235,7 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
     } while (0)
 #define WASABI_CONSUME(s)                                                                   \
     do {                                                                                    \
-        const int base = (rb[s] << 9) >> 9;                                                 \
-        const int addr = ((int)(rw[s] & 0xffffu) << ((unsigned)rb[s] >> 23)) + base;        \
+        const int addr = (int)((rw[s] >> 14) & 0x3fffu) * S + (int)(rw[s] & 0x3fffu) + rb[s]; \
         const uint32_t sa = (unsigned)(addr - sub_lo) < (unsigned)(Th * S)                  \
                                 ? tile_sa + 8u * (uint32_t)addr : dummy_sa;                 \
         float2 o = lds2(sa);                                                                \

@@ -173,8 +173,7 @@ __global__ void select_init_kernel(const void *tables, SelState *st, int n_depth
 }
 
 // K2c: per (depth, level, band, Xb) group, count (pass 0) or scatter (pass 1) the kept
-// coefficients in (Yb, subband) order.  Entry record: value float2 + packed position
-// pos = w | (u << 16), u = 2 (Yb - band hb) + sby, v = 2 Xb + sbx, w = u S + v.
+// coefficients in (Yb, subband) order as 16-byte entries (internal.h pack_entry_pos).
 __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 *__restrict__ coef_val,
                                                      const uint32_t *__restrict__ coef_key,
                                                      const SelState *__restrict__ st, int n_depth, int L, int T,
@@ -207,11 +206,9 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
     const unsigned long long thr = st[d].prefix;
     const int st_px = 1 << (l - 1);
     const int yb1 = min(band * hb + hb, nb);
-    const int S = h.S;
     int out = pass ? ptr[g] : 0;
     int cnt = 0;
-    float2 *val = atw<float2>(tables, h.val_off);
-    uint32_t *pos = atw<uint32_t>(tables, h.pos_off);
+    uint4 *ent = atw<uint4>(tables, h.ent_off);
     for (int Yb = band * hb; Yb < yb1; Yb++) {
         for (int sb = (l == L ? 0 : 1); sb < 4; sb++) {
             const int sbx = sb & 1, sby = sb >> 1;
@@ -221,9 +218,8 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
             const unsigned long long key = ((unsigned long long)coef_key[o] << 32) | (unsigned long long)(~lin);
             if (key >= thr) {
                 if (pass) {
-                    const int u = 2 * (Yb - band * hb) + sby, v = 2 * Xb + sbx;
-                    val[out] = coef_val[o];
-                    pos[out] = (uint32_t)(u * S + v) | ((uint32_t)u << 16);
+                    const float2 v = coef_val[o];
+                    ent[out] = make_uint4(pack_entry_pos(X, Y, l), __float_as_uint(v.x), __float_as_uint(v.y), 0u);
                     out++;
                 }
                 cnt++;

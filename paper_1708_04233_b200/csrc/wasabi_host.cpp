@@ -211,8 +211,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     h.ddesc_off = off; off = align_up(off + sizeof(DDesc) * g.nd, 256);
     h.ctabase_off = off; off = align_up(off + 4 * (g.nd + 1), 256);
     h.ptr_off = off; off = align_up(off + 4 * (size_t)(ptr + 1), 256);
-    h.pos_off = off; off = align_up(off + 4 * (size_t)entries, 256);
-    h.val_off = off; off = align_up(off + 8 * (size_t)entries, 256);
+    h.ent_off = off; off = align_up(off + 16 * (size_t)entries, 256);
     h.table_bytes = off;
     g.table_bytes = off;
     // build scratch
@@ -499,32 +498,18 @@ wasabi_status wasabi_export_table(const wasabi_params *params, const void *d_tab
     if (n != D.n_r) return fail(WASABI_ESTATE, "depth %d holds %lld entries, expected N_r = %lld", depth,
                                 (long long)n, (long long)D.n_r);
     if (cap < n) return fail(WASABI_ENOSPC, "need capacity %lld", (long long)n);
-    std::vector<uint32_t> pos(n);
-    std::vector<float> val(2 * n);
-    if (n) {
-        CK(cudaMemcpy(pos.data(), tb + g.th.pos_off + 4 * (size_t)e0, 4 * (size_t)n, cudaMemcpyDeviceToHost), "read pos");
-        CK(cudaMemcpy(val.data(), tb + g.th.val_off + 8 * (size_t)e0, 8 * (size_t)n, cudaMemcpyDeviceToHost), "read val");
-    }
+    std::vector<uint32_t> ent(4 * (size_t)n);
+    if (n)
+        CK(cudaMemcpy(ent.data(), tb + g.th.ent_off + 16 * (size_t)e0, 16 * (size_t)n, cudaMemcpyDeviceToHost),
+           "read entries");
     struct Rec { int32_t l, Y, X; int64_t i; };
     std::vector<Rec> rec;
     rec.reserve(n);
-    const int64_t H = K.H;
-    for (int l = 1; l <= g.L; l++) {
-        const int64_t nb = (2 * H) >> l, hb = band_blocks(g.T, l), nbands = (nb + hb - 1) / hb;
-        const int64_t gl = K.ptr_base[l - 1] - D.group_base;
-        for (int64_t band = 0; band < nbands; band++)
-            for (int64_t Xb = 0; Xb < nb; Xb++) {
-                const int64_t gi = gl + band * (nb + 1) + Xb;
-                for (int64_t i = ptr[gi]; i < ptr[gi + 1]; i++) {
-                    const uint32_t p = pos[i - e0];
-                    const int64_t u = p >> 16, w = p & 0xffff, v = w - u * g.S;
-                    const int64_t Xb2 = v >> 1, sbx = v & 1, Yb = band * hb + (u >> 1), sby = u & 1;
-                    if (Xb2 != Xb) return fail(WASABI_ESTATE, "corrupt position record");
-                    rec.push_back(Rec{l, (int32_t)((Yb << l) + sby * (1 << (l - 1))),
-                                      (int32_t)((Xb2 << l) + sbx * (1 << (l - 1))), i - e0});
-                }
-            }
+    for (int64_t i = 0; i < n; i++) {
+        const uint32_t p = ent[4 * i];
+        rec.push_back(Rec{(int32_t)(p >> 28), (int32_t)((p >> 14) & 0x3fff), (int32_t)(p & 0x3fff), i});
     }
+    const int64_t H = K.H;
     std::sort(rec.begin(), rec.end(), [](const Rec &a, const Rec &b) {
         if (a.l != b.l) return a.l < b.l;
         if (a.Y != b.Y) return a.Y < b.Y;
@@ -534,7 +519,10 @@ wasabi_status wasabi_export_table(const wasabi_params *params, const void *d_tab
         if (h_level) h_level[k] = rec[k].l;
         if (h_dx) h_dx[k] = (int32_t)(rec[k].X - H);
         if (h_dy) h_dy[k] = (int32_t)(rec[k].Y - H);
-        if (h_val) { h_val[2 * k] = val[2 * rec[k].i]; h_val[2 * k + 1] = val[2 * rec[k].i + 1]; }
+        if (h_val) {
+            memcpy(&h_val[2 * k], &ent[4 * rec[k].i + 1], 4);
+            memcpy(&h_val[2 * k + 1], &ent[4 * rec[k].i + 2], 4);
+        }
     }
     return WASABI_OK;
 }
