@@ -193,12 +193,13 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(args.warmup):
-        pl.run(d_pts)
+        pl.run(d_pts, fused=not args.unfused)
     torch.cuda.synchronize(dev)
     st = W.bins_stats(pl.bins)
 
-    stages = ["tables", "bin", "superpose", "inverse_quantize"]
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    stages = ["tables", "bin", "superpose", "inverse_quantize"] if args.unfused else \
+        ["tables", "bin", "superpose_inverse_quantize"]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
     clocks = Clocks(local, os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
                     if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_rank{rank}.csv")
     barrier()
@@ -213,15 +214,19 @@ def run_ours(args, cfg):
         e[1].record(stream)
         pl.bin(d_pts)
         e[2].record(stream)
-        pl.superpose()
-        e[3].record(stream)
-        pl.inverse()
-        e[4].record(stream)
+        if args.unfused:
+            pl.superpose()
+            e[3].record(stream)
+            pl.inverse()
+            e[4].record(stream)
+        else:
+            pl.superpose_inverse()
+            e[3].record(stream)
     torch.cuda.synchronize(dev)
     launches = W.kernel_launches() - launches0
     barrier()
     ck = clocks.stop()
-    total_ms = sum(ev[k][0].elapsed_time(ev[k][4]) for k in range(args.steps))
+    total_ms = sum(ev[k][0].elapsed_time(ev[k][len(stages)]) for k in range(args.steps))
     stage_ms = {s: statistics.mean(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(args.steps))
                 for i, s in enumerate(stages)}
     t_ms = max_over_ranks(total_ms)
@@ -242,6 +247,7 @@ def run_ours(args, cfg):
     rows = row1 - row0
     alg = {"superpose": 8.0 * rows * cfg.n_h + 16.0 * st["n_valid"],
            "inverse_quantize": 16.125 * rows * cfg.n_h,
+           "superpose_inverse_quantize": 8.125 * rows * cfg.n_h + 16.0 * st["n_valid"],
            "bin": 16.0 * n + 16.0 * st["n_valid"] + 8.0 * st["entries"],
            "tables": 0.0}
     dom = max(stage_ms, key=stage_ms.get)
@@ -253,7 +259,7 @@ def run_ours(args, cfg):
         except Exception:
             traffic = None
     ach = alg[dom] / (stage_ms[dom] * 1e-3) / 1e9 if alg[dom] else 0.0
-    step_bytes = 24.125 * rows * cfg.n_h + 32.0 * n
+    step_bytes = (24.125 if args.unfused else 8.125) * rows * cfg.n_h + 32.0 * n
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
                 "step_achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,
@@ -293,7 +299,7 @@ def run_ours(args, cfg):
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded generators, inputs/; the paper's 3D model is unavailable)",
-               "config": {"workload": _workload(cfg), "n_h": cfg.n_h, "n_points": n, "levels": cfg.levels,
+               "config": {"workload": _workload(cfg), "path": "unfused" if args.unfused else "fused", "n_h": cfg.n_h, "n_points": n, "levels": cfg.levels,
                           "retention": cfg.retention, "n_depth": cfg.n_depth, "tile": p.tile,
                           "rows_per_gpu": rows, "parallelism": f"row bands x{world}",
                           "l2": f"inputs larger than L2 (psi/u {8 * rows * cfg.n_h / 1e9:.1f} GB per GPU per step)"},
@@ -318,6 +324,7 @@ def main():
     ap.add_argument("--tile", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--unfused", action="store_true", help="time the 4-call path (psi through HBM)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.points:

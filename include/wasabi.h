@@ -128,6 +128,15 @@ wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_table
 wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables, const void *d_bins,
                                int64_t row0, int64_t row1, float *d_psi, cudaStream_t stream);
 
+/* Steps 2b + 3 (+ 4) fused (PAPER.md:93-94 run back to back): each tile's
+ * psi is superposed, inverse-transformed and quantised in shared memory and never written to HBM.
+ * Results are bit-identical to wasabi_superpose followed by wasabi_inverse_wt.
+ * d_u: (row1 - row0) x n_h complex64 or NULL (print only); d_bits as in wasabi_quantize or NULL
+ * (then `print` may be NULL). */
+wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *d_tables, const void *d_bins,
+                                       int64_t row0, int64_t row1, const wasabi_print_params *print, float *d_u,
+                                       uint8_t *d_bits, cudaStream_t stream);
+
 /* ---------------------------------------------------------------- steps 3 (+4) */
 
 /* Step 3: L-level inverse Haar, tile-local (band rows multiples of 2^L, so
@@ -150,7 +159,7 @@ wasabi_status wasabi_hologram_workspace_bytes(const wasabi_params *params, int64
                                               int64_t row1, size_t *workspace_bytes);
 
 /* Whole hot path from HOST buffers: H2D copy of h_points (n x 4 float32), steps 1-4 for band
- * [row0, row1), D2H copy of the bits (h_bits, (row1-row0) x n_h/8 bytes) and, if h_u != NULL,
+ * [row0, row1) (steps 2b-4 through wasabi_superpose_inverse), D2H copy of the bits (h_bits, (row1-row0) x n_h/8 bytes) and, if h_u != NULL,
  * of u ((row1-row0) x n_h complex64).  Host buffers should be pinned for asynchronous copies.
  * Returns after enqueueing; the caller synchronises `stream` before reading h_bits / h_u. */
 wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_print_params *print,

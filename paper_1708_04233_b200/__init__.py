@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
             "wasabi_bin_points_bytes": [_PP, _i64, _i64, _i64, C.POINTER(_sz)],
             "wasabi_bin_points": [_PP, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp],
             "wasabi_superpose": [_PP, _vp, _vp, _i64, _i64, _vp, _vp],
+            "wasabi_superpose_inverse": [_PP, _vp, _vp, _i64, _i64, _PR, _vp, _vp, _vp],
             "wasabi_inverse_wt": [_PP, _vp, _vp, _i64, _i64, _PR, _vp, _vp],
             "wasabi_quantize": [_PP, _PR, _vp, _i64, _i64, _vp, _vp],
             "wasabi_hologram_workspace_bytes": [_PP, _i64, _i64, _i64, C.POINTER(_sz)],
@@ -187,6 +188,14 @@ def bin_points(p: Params, tables, points, row0: int, row1: int, bins, stream=Non
 def superpose(p: Params, tables, bins, row0: int, row1: int, psi, stream=None):
     _check(lib().wasabi_superpose(C.byref(p.c()), _ptr(tables), _ptr(bins), row0, row1, _ptr(psi),
                                   _stream(stream)))
+
+
+def superpose_inverse(p: Params, tables, bins, row0: int, row1: int, print_params: Optional[PrintParams], u,
+                      bits=None, stream=None):
+    """Steps 2b-4 fused: psi stays in shared memory; writes u (may be None) and bits (may be None)."""
+    pr = C.byref(print_params.c()) if print_params is not None else None
+    _check(lib().wasabi_superpose_inverse(C.byref(p.c()), _ptr(tables), _ptr(bins), row0, row1, pr, _ptr(u),
+                                          _ptr(bits), _stream(stream)))
 
 
 # ----------------------------------------------------------------------------- steps 3, 4

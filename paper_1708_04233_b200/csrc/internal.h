@@ -93,8 +93,11 @@ size_t scan_scratch_bytes(int64_t n);
 cudaError_t launch_bin(const BinHeader &bh, void *d_bins, const KDesc *kd, const float4 *pts,
                        double pitch, int64_t n_h, double z_min, double dz, int n_depth, cudaStream_t s);
 
-cudaError_t launch_superpose_v1(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x,
-                                int tiles_y, int64_t row0, int64_t n_h, float2 *psi, cudaStream_t s);
+// fused = 0: write psi; fused = 1: inverse Haar in shared memory, write u (psi pointer, may be NULL)
+// and, if bits != NULL, the print bits (print4 = {xr, yr, zr, 1/lambda}).
+cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x, int tiles_y,
+                             int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
+                             uint8_t *bits, cudaStream_t s);
 cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStream_t s);
 
 cudaError_t launch_inverse(const float2 *psi, float2 *u, int64_t rows, int64_t n_h, int64_t row0, int levels,

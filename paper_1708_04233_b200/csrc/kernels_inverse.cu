@@ -13,25 +13,10 @@
 #include <cstdint>
 
 #include "internal.h"
+#include "device_common.cuh"
 
 namespace wasabi {
 namespace {
-
-struct QArgs {
-    double xr, yr, zr2, inv_lambda, pitch;
-    int64_t half;  // N_h / 2
-};
-
-__device__ __forceinline__ float interference(float2 u, int64_t X, int64_t Y, const QArgs &q) {
-    const double x = (double)(X - q.half) * q.pitch, y = (double)(Y - q.half) * q.pitch;
-    const double dx = x - q.xr, dy = y - q.yr;
-    const double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), q.zr2));
-    const double cyc = r * q.inv_lambda;
-    const float f = (float)(cyc - rint(cyc));  // in [-1/2, 1/2]
-    float s, c;
-    sincospif(2.0f * f, &s, &c);
-    return fmaf(u.x, c, u.y * s);
-}
 
 constexpr int kT = 64;
 constexpr int kS = kT + 2;  // float2 row stride (keeps float4 alignment of rows)
@@ -50,25 +35,7 @@ __global__ void __launch_bounds__(256) inverse_kernel(const float2 *psi, float2 
         *reinterpret_cast<float4 *>(&s[row * kS + 2 * c4]) = v;
     }
     __syncthreads();
-    for (int l = L; l >= 1; l--) {
-        const int st = 1 << (l - 1), nq = kT >> l;
-        for (int qd = threadIdx.x; qd < nq * nq; qd += 256) {
-            const int bx = (qd % nq) << l, by = (qd / nq) << l;
-            float2 *pa = &s[by * kS + bx], *pb = pa + st, *pc = pa + st * kS, *pd = pc + st;
-            const float2 LL = *pa, HL = *pb, LH = *pc, HH = *pd;
-            float2 A, B, C, D;
-            A.x = ((LL.x + HL.x) + (LH.x + HH.x)) * 0.5f;
-            B.x = ((LL.x - HL.x) + (LH.x - HH.x)) * 0.5f;
-            C.x = ((LL.x + HL.x) - (LH.x + HH.x)) * 0.5f;
-            D.x = ((LL.x - HL.x) - (LH.x - HH.x)) * 0.5f;
-            A.y = ((LL.y + HL.y) + (LH.y + HH.y)) * 0.5f;
-            B.y = ((LL.y - HL.y) + (LH.y - HH.y)) * 0.5f;
-            C.y = ((LL.y + HL.y) - (LH.y + HH.y)) * 0.5f;
-            D.y = ((LL.y - HL.y) - (LH.y - HH.y)) * 0.5f;
-            *pa = A; *pb = B; *pc = C; *pd = D;
-        }
-        __syncthreads();
-    }
+    inverse_haar_tile(s, kT, kS, L, threadIdx.x, 256);
     if (write_u) {
         float4 *dst = reinterpret_cast<float4 *>(u);
 #pragma unroll
@@ -118,22 +85,11 @@ __global__ void __launch_bounds__(256) quantize_kernel(const float2 *__restrict_
     }
 }
 
-QArgs make_q(const double *print4, double pitch, int64_t n_h) {
-    QArgs q;
-    q.xr = print4 ? print4[0] : 0.0;
-    q.yr = print4 ? print4[1] : 0.0;
-    q.zr2 = print4 ? print4[2] * print4[2] : 0.0;
-    q.inv_lambda = print4 ? print4[3] : 0.0;
-    q.pitch = pitch;
-    q.half = n_h / 2;
-    return q;
-}
-
 }  // namespace
 
 cudaError_t launch_inverse(const float2 *psi, float2 *u, int64_t rows, int64_t n_h, int64_t row0, int levels,
                            const double *print4, double pitch, uint8_t *bits, cudaStream_t s) {
-    const QArgs q = make_q(print4, pitch, n_h);
+    const QArgs q = make_qargs(print4, pitch, n_h);
     dim3 grid((unsigned)(n_h / kT), (unsigned)(rows / kT));
     if (grid.x == 0 || grid.y == 0) return cudaSuccess;
     count_launches(1);
@@ -143,7 +99,7 @@ cudaError_t launch_inverse(const float2 *psi, float2 *u, int64_t rows, int64_t n
 
 cudaError_t launch_quantize(const float2 *u, int64_t rows, int64_t n_h, int64_t row0, const double *print4,
                             double pitch, uint8_t *bits, cudaStream_t s) {
-    const QArgs q = make_q(print4, pitch, n_h);
+    const QArgs q = make_qargs(print4, pitch, n_h);
     const int64_t nbytes = rows * (n_h / 8);
     if (nbytes == 0) return cudaSuccess;
     const int64_t blocks = std::min<int64_t>((nbytes + 255) / 256, 148 * 64);

@@ -23,6 +23,7 @@
 #include <cstdint>
 
 #include "internal.h"
+#include "device_common.cuh"
 
 namespace wasabi {
 namespace {
@@ -55,7 +56,8 @@ __device__ __forceinline__ bool in_class(int c, int l) { return c == 0 ? (l == 1
 template <int SEGW>
 __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restrict__ d_bins,
                                                            const void *__restrict__ d_tables, SupArgs A,
-                                                           float2 *__restrict__ psi) {
+                                                           float2 *__restrict__ psi, int fused, QArgs qa,
+                                                           uint8_t *__restrict__ bits) {
     constexpr int PPS = 32 / SEGW;            // points per range step
     constexpr int kH = kPB / PPS;             // range steps per batch
     extern __shared__ float2 tile[];          // T x S (+4 scratch)
@@ -262,6 +264,26 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
 #undef WASABI_PREFETCH
 #undef WASABI_CONSUME
     __syncthreads();
+    if (fused) {
+        // steps 3 (+4) in place: psi never leaves shared memory
+        inverse_haar_tile(tile, T, S, A.L, threadIdx.x, 128);
+        if (bits) {
+            const int bpr = T / 8;
+            for (int bi = threadIdx.x; bi < T * bpr; bi += 128) {
+                const int row = bi / bpr, xb = bi % bpr;
+                const int64_t Y = tile_y0 + row;
+                unsigned byte = 0;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int x = xb * 8 + i;
+                    const float I = interference(tile[row * S + x], tile_x0 + x, Y, qa);
+                    byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
+                }
+                bits[(Y - A.row0) * (A.n_h / 8) + tile_x0 / 8 + xb] = (uint8_t)byte;
+            }
+        }
+        if (!psi) return;
+    }
     float2 *out = psi + (int64_t)(tile_y0 - A.row0) * A.n_h + tile_x0;
     for (int y = wid; y < T; y += 4)
         for (int x = lane; x < T; x += 32) out[(int64_t)y * A.n_h + x] = tile[y * S + x];
@@ -269,8 +291,9 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
 
 }  // namespace
 
-cudaError_t launch_superpose_v1(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x,
-                                int tiles_y, int64_t row0, int64_t n_h, float2 *psi, cudaStream_t s) {
+cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x, int tiles_y,
+                             int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
+                             uint8_t *bits, cudaStream_t s) {
     const int smem = (T * S + 4) * (int)sizeof(float2);
     // range slots per (class, row half) and point: <= 8 for T = 64, <= 16 for T = 128
     auto kern = T <= 64 ? superpose_kernel<8> : superpose_kernel<16>;
@@ -281,7 +304,8 @@ cudaError_t launch_superpose_v1(const void *d_bins, const void *d_tables, int T,
     const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
     if (n_tiles > 0) {
         count_launches(1);
-        kern<<<(unsigned)n_tiles, 128, smem, s>>>(d_bins, d_tables, A, psi);
+        kern<<<(unsigned)n_tiles, 128, smem, s>>>(d_bins, d_tables, A, psi, fused,
+                                                  make_qargs(print4, pitch, n_h), bits);
     }
     return cudaGetLastError();
 }

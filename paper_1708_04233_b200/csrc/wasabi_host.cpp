@@ -362,9 +362,29 @@ wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables
     if (!d_tables || !d_bins || (!d_psi && row1 > row0)) return fail(WASABI_EINVAL, "NULL buffer");
     if (!aligned(d_psi, 16)) return fail(WASABI_EINVAL, "d_psi must be 16-byte aligned");
     const int T = params->tile;
-    CK(launch_superpose_v1(d_bins, d_tables, T, T + 1, params->levels, (int)(params->n_h / T),
-                           (int)((row1 - row0) / T), row0, params->n_h, reinterpret_cast<float2 *>(d_psi), stream),
+    CK(launch_superpose(d_bins, d_tables, T, T + 1, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
+                        row0, params->n_h, reinterpret_cast<float2 *>(d_psi), 0, nullptr, params->pitch_m, nullptr,
+                        stream),
        "superpose");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *d_tables, const void *d_bins,
+                                       int64_t row0, int64_t row1, const wasabi_print_params *print, float *d_u,
+                                       uint8_t *d_bits, cudaStream_t stream) {
+    wasabi_status st = validate(params);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (!d_tables || !d_bins) return fail(WASABI_EINVAL, "NULL buffer");
+    if (d_bits && !print) return fail(WASABI_EINVAL, "d_bits needs print params");
+    if (!aligned(d_u, 16)) return fail(WASABI_EINVAL, "d_u must be 16-byte aligned");
+    double p4[4];
+    if (print) { p4[0] = print->x_r_m; p4[1] = print->y_r_m; p4[2] = print->z_r_m; p4[3] = 1.0 / params->wavelength_m; }
+    const int T = params->tile;
+    CK(launch_superpose(d_bins, d_tables, T, T + 1, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
+                        row0, params->n_h, reinterpret_cast<float2 *>(d_u), 1, print ? p4 : nullptr, params->pitch_m,
+                        d_bits, stream),
+       "superpose_inverse");
     return WASABI_OK;
 }
 
@@ -456,8 +476,9 @@ wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_pri
         return st;
     if ((st = wasabi_bin_points(params, ws + w.tables, d_pts, n, row0, row1, ws + w.bins, w.bin_bytes, stream)))
         return st;
-    if ((st = wasabi_superpose(params, ws + w.tables, ws + w.bins, row0, row1, d_field, stream))) return st;
-    if ((st = wasabi_inverse_wt(params, d_field, d_field, row0, row1, print, d_bits, stream))) return st;
+    if ((st = wasabi_superpose_inverse(params, ws + w.tables, ws + w.bins, row0, row1, print, h_u ? d_field : nullptr,
+                                       d_bits, stream)))
+        return st;
     const size_t nbits = (size_t)(row1 - row0) * (size_t)(params->n_h / 8);
     if (h_bits && nbits) CK(cudaMemcpyAsync(h_bits, d_bits, nbits, cudaMemcpyDeviceToHost, stream), "D2H bits");
     if (h_u && row1 > row0)

@@ -7,14 +7,15 @@ from __future__ import annotations
 from typing import Optional
 
 from . import (Params, PrintParams, bin_points, bin_points_bytes, build_psf_tables, inverse_wt,
-               psf_tables_bytes, quantize, superpose)
+               psf_tables_bytes, quantize, superpose, superpose_inverse)
 
 
 class Pipeline:
     """Device buffers for band [row0, row1) of a hologram with params `p` and up to n_max points.
 
-    run(points) executes: build tables (step 1) -> bin (2a) -> superpose (2b) -> inverse (3),
-    fused with quantise (4) when `bits` is requested.  `u` is written in place over psi.
+    run(points) executes: build tables (step 1) -> bin (2a) -> fused superpose + inverse + quantise
+    (2b-4, psi never leaves shared memory); run(points, fused=False) runs the unfused four-call path
+    (superpose writes psi, the inverse overwrites it in place with u).
     """
 
     def __init__(self, p: Params, n_max: int, row0: int = 0, row1: Optional[int] = None, device=None,
@@ -63,10 +64,18 @@ class Pipeline:
     def quantize(self):
         quantize(self.p, self.print_params, self.field, self.row0, self.row1, self.bits, self.stream)
 
-    def run(self, points, build_tables: bool = True):
+    def superpose_inverse(self):
+        u = self.field if self.want_u else None
+        superpose_inverse(self.p, self.tables, self.bins, self.row0, self.row1, self.print_params, u, self.bits,
+                          self.stream)
+
+    def run(self, points, build_tables: bool = True, fused: bool = True):
         if build_tables or not self.tables_built:
             self.build_tables()
         self.bin(points)
-        self.superpose()
-        self.inverse()
+        if fused:
+            self.superpose_inverse()
+        else:
+            self.superpose()
+            self.inverse()
         return self.field, self.bits

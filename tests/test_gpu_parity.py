@@ -254,6 +254,28 @@ def test_fused_equals_standalone_quantize(W):
     assert np.array_equal(bits.cpu().numpy(), bits_fused)
 
 
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", {}), ("C1", dict(levels=1)), ("C1", dict(tile=128, levels=6))])
+def test_fused_superpose_inverse_bitwise(W, name, kw):
+    """NEXT-1 fused kernel == superpose + inverse_wt (+ fused quantise), bit for bit; print-only too."""
+    import torch
+    cfg = CONFIGS[name].replace(**kw)
+    pts = make_points(cfg, n=3000)
+    p = gpu_params(cfg)
+    pl = W.Pipeline(p, len(pts), 0, p.n_h)
+    d = torch.from_numpy(pts).cuda()
+    pl.run(d, fused=False)
+    u_ref, b_ref = pl.field.clone(), pl.bits.clone()
+    pl.field.zero_()
+    pl.bits.zero_()
+    pl.run(d, fused=True)
+    torch.cuda.synchronize()
+    assert torch.equal(pl.field, u_ref) and torch.equal(pl.bits, b_ref)
+    pl.bits.zero_()
+    W.superpose_inverse(p, pl.tables, pl.bins, 0, p.n_h, pl.print_params, None, pl.bits)
+    torch.cuda.synchronize()
+    assert torch.equal(pl.bits, b_ref)
+
+
 # ---------------------------------------------------------------- whole path from host buffers
 def test_hologram_host_equals_device_path(W):
     import torch
