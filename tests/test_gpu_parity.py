@@ -328,3 +328,46 @@ def test_c4_full_size_sampled(W, orc):
     for t in rng.integers(0, len(ptr_g) - 1, 8):
         X0, Y0 = int(t % tiles_x) * T, int(t // tiles_x) * T
         assert np.array_equal(idx_g[ptr_g[t]:ptr_g[t + 1]], orc.bin_tile(P, T, pts, X0, Y0))
+
+
+# ---------------------------------------------------------------- C5 (BASELINE configs[4])
+@pytest.mark.parametrize("r", [0.01, 0.25, 1.0])
+def test_c5_band_parity(W, orc, r):
+    """C5 (16,384^2, z ~ U[0.1,1] mm, 64 levels, L=5) at N=1e4 on a 256-row band; oracle on a
+    2048-wide window of it."""
+    cfg = CONFIGS["C5"].replace(retention=r)
+    pts = make_points(cfg, n=10_000)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 8192, 8448)
+    _check_fields(orc, cfg, pts, 8192, 8448, pl, psi_g, u_g, bits_g, x0=7168, w=2048)
+
+
+def test_c5_aligned_keep_all_equals_direct_sum(W, orc):
+    """r=100%, 2^L-aligned points on levels at C5 scale: u equals the quantised direct sum (D2)."""
+    cfg = CONFIGS["C5"].replace(retention=1.0, aligned=True, kind="levels")
+    pts = make_points(cfg, n=2000)
+    pl, psi_g, u_g, bits_g = _gpu_run(W, cfg, pts, 4096, 4352)
+    P = orc_params(orc, cfg)
+    d2 = orc.direct_d2(P, pts.astype(np.float64), 6144, 4096, 1024, 256)
+    assert rel_l2(u_g[:, 6144:7168], d2) <= 1e-5
+
+
+def test_c5_full_size_sampled(W, orc):
+    """C5 at N=1e6, r=5% on the full 16,384^2 hologram; sampled 32x32 blocks recomputed by the oracle."""
+    import torch
+    cfg = CONFIGS["C5"]
+    pts = make_points(cfg, n=1_000_000)
+    p = gpu_params(cfg)
+    pl = W.Pipeline(p, len(pts), 0, p.n_h)
+    pl.run(torch.from_numpy(pts).cuda())
+    torch.cuda.synchronize()
+    assert W.bins_stats(pl.bins)["status"] == 0
+    P = orc_params(orc, cfg)
+    lut = orc.Lut(P)
+    rng = np.random.default_rng(55)
+    B = 32
+    for _ in range(4):
+        X0 = int(rng.integers(0, p.n_h // B)) * B
+        Y0 = int(rng.integers(0, p.n_h // B)) * B
+        u_o, _, _ = lut.hologram_window(pts, X0, Y0, B, B)
+        u_g = field_np(pl.field[Y0:Y0 + B, X0:X0 + B])
+        assert rel_l2(u_g, u_o) <= 1e-5
