@@ -152,6 +152,19 @@ wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi,
 wasabi_status wasabi_quantize(const wasabi_params *params, const wasabi_print_params *print, const float *d_u,
                               int64_t row0, int64_t row1, uint8_t *d_bits, cudaStream_t stream);
 
+/* ---------------------------------------------------------------- conventional baseline */
+
+/* The conventional method the paper compares against (N-LUT), on the GPU:
+ * the quantised direct sum of Eq.(1) by stamping the same (untransformed) PSF tables,
+ * u(X, Y) = sum_j a_j f_{iz_j}(X - ix_j, Y - iy_j) -- WASABI without the shrinkage.  It is the
+ * reference for the PSNR of the C5 sweep (reading R-A18) and the same-box speed-up baseline.
+ * Dense tables: one (2H_d)^2 complex64 table per depth (caller-owned buffer). */
+wasabi_status wasabi_psf_dense_bytes(const wasabi_params *params, size_t *bytes);
+wasabi_status wasabi_build_psf_dense(const wasabi_params *params, void *d_dense, size_t bytes, cudaStream_t stream);
+/* d_bins from wasabi_bin_points for the same band; d_u: (row1 - row0) x n_h complex64, overwritten. */
+wasabi_status wasabi_direct_sum(const wasabi_params *params, const void *d_dense, const void *d_bins, int64_t row0,
+                                int64_t row1, float *d_u, cudaStream_t stream);
+
 /* ---------------------------------------------------------------- whole path, host buffers */
 
 /* Device workspace for wasabi_hologram_host (tables + scratch + points + bins + field). */

@@ -105,6 +105,9 @@ def lib() -> C.CDLL:
             "wasabi_quantize": [_PP, _PR, _vp, _i64, _i64, _vp, _vp],
             "wasabi_hologram_workspace_bytes": [_PP, _i64, _i64, _i64, C.POINTER(_sz)],
             "wasabi_hologram_host": [_PP, _PR, _vp, _i64, _i64, _i64, _vp, _sz, _vp, _vp, _vp],
+            "wasabi_psf_dense_bytes": [_PP, C.POINTER(_sz)],
+            "wasabi_build_psf_dense": [_PP, _vp, _sz, _vp],
+            "wasabi_direct_sum": [_PP, _vp, _vp, _i64, _i64, _vp, _vp],
             "wasabi_tables_check": [_PP, _vp],
             "wasabi_export_table": [_PP, _vp, C.c_int32, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
             "wasabi_export_bins": [_PP, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
@@ -209,6 +212,22 @@ def inverse_wt(p: Params, psi, u, row0: int, row1: int, print_params: Optional[P
 def quantize(p: Params, print_params: PrintParams, u, row0: int, row1: int, bits, stream=None):
     _check(lib().wasabi_quantize(C.byref(p.c()), C.byref(print_params.c()), _ptr(u), row0, row1, _ptr(bits),
                                  _stream(stream)))
+
+
+# ----------------------------------------------------------------------------- conventional baseline
+def psf_dense_bytes(p: Params) -> int:
+    b = _sz()
+    _check(lib().wasabi_psf_dense_bytes(C.byref(p.c()), C.byref(b)))
+    return b.value
+
+
+def build_psf_dense(p: Params, dense, stream=None):
+    _check(lib().wasabi_build_psf_dense(C.byref(p.c()), _ptr(dense), _nbytes(dense), _stream(stream)))
+
+
+def direct_sum(p: Params, dense, bins, row0: int, row1: int, u, stream=None):
+    """Quantised direct sum of Eq.(1) (PSF stamping; the paper's conventional method) for a band."""
+    _check(lib().wasabi_direct_sum(C.byref(p.c()), _ptr(dense), _ptr(bins), row0, row1, _ptr(u), _stream(stream)))
 
 
 # ----------------------------------------------------------------------------- whole path

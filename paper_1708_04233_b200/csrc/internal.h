@@ -70,6 +70,14 @@ __host__ __device__ inline int band_blocks(int T, int l) {
     return hb < 1 ? 1 : hb;
 }
 
+// Dense (untransformed) PSF table of one depth, for the direct-sum stamping kernel (32 bytes).
+struct DenseDesc {
+    double z, R;
+    int64_t off;       // element offset of the (side x side) complex64 table
+    int32_t side;      // 2H
+    int32_t cta_base;  // prefix of 64x64 build CTAs
+};
+
 // ---- table geometry computed on host (L0) ----
 struct LevelGeom {
     int nb, hb, nbands;   // blocks per row, band height (blocks), bands
@@ -99,6 +107,11 @@ cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, in
                              int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
                              uint8_t *bits, cudaStream_t s);
 cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStream_t s);
+
+cudaError_t launch_psf_dense(const DenseDesc *d_desc, int n_depth, float2 *out, double k, double pitch,
+                             int64_t total_ctas, cudaStream_t s);
+cudaError_t launch_stamp(const void *d_bins, const DenseDesc *d_desc, const float2 *dense, int tiles_x, int tiles_y,
+                         int64_t row0, int64_t n_h, int T, float2 *u, cudaStream_t s);
 
 cudaError_t launch_inverse(const float2 *psi, float2 *u, int64_t rows, int64_t n_h, int64_t row0, int levels,
                            const double *print4 /* xr, yr, zr, inv_lambda or NULL */, double pitch,

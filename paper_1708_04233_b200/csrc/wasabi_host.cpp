@@ -420,6 +420,72 @@ wasabi_status wasabi_quantize(const wasabi_params *params, const wasabi_print_pa
     return WASABI_OK;
 }
 
+// ---------------------------------------------------------------- conventional baseline (direct sum)
+
+namespace {
+struct DenseLayout {
+    std::vector<DenseDesc> dd;
+    size_t data_off = 0, bytes = 0;
+    int64_t ctas = 0;
+};
+DenseLayout dense_layout(const Geo &g) {
+    DenseLayout L;
+    L.dd.resize(g.nd);
+    int64_t off = 0, ctas = 0;
+    for (int d = 0; d < g.nd; d++) {
+        DenseDesc &D = L.dd[d];
+        D.z = g.dd[d].z; D.R = g.dd[d].R; D.side = g.dd[d].side; D.off = off; D.cta_base = (int32_t)ctas;
+        off += (int64_t)D.side * D.side;
+        const int64_t t = (D.side + 63) / 64;
+        ctas += t * t;
+    }
+    L.ctas = ctas;
+    L.data_off = align_up(sizeof(DenseDesc) * g.nd, 256);
+    L.bytes = L.data_off + 8 * (size_t)off;
+    return L;
+}
+}  // namespace
+
+wasabi_status wasabi_psf_dense_bytes(const wasabi_params *params, size_t *bytes) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if (bytes) *bytes = dense_layout(g).bytes;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_build_psf_dense(const wasabi_params *params, void *d_dense, size_t bytes, cudaStream_t stream) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    DenseLayout L = dense_layout(g);
+    if (!d_dense || !aligned(d_dense, 256)) return fail(WASABI_EINVAL, "d_dense NULL or not 256-byte aligned");
+    if (bytes < L.bytes) return fail(WASABI_ENOSPC, "dense table buffer needs %zu bytes", L.bytes);
+    char *b = static_cast<char *>(d_dense);
+    CK(launch_write_blob(b, L.dd.data(), sizeof(DenseDesc) * g.nd, stream), "write dense desc");
+    CK(launch_psf_dense(reinterpret_cast<const DenseDesc *>(b), g.nd, reinterpret_cast<float2 *>(b + L.data_off), g.k,
+                        params->pitch_m, L.ctas, stream),
+       "psf_dense");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_direct_sum(const wasabi_params *params, const void *d_dense, const void *d_bins, int64_t row0,
+                                int64_t row1, float *d_u, cudaStream_t stream) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (!d_dense || !d_bins || (!d_u && row1 > row0)) return fail(WASABI_EINVAL, "NULL buffer");
+    DenseLayout L = dense_layout(g);
+    const char *b = static_cast<const char *>(d_dense);
+    const int T = params->tile;
+    CK(launch_stamp(d_bins, reinterpret_cast<const DenseDesc *>(b), reinterpret_cast<const float2 *>(b + L.data_off),
+                    (int)(params->n_h / T), (int)((row1 - row0) / T), row0, params->n_h, T,
+                    reinterpret_cast<float2 *>(d_u), stream),
+       "direct_sum");
+    return WASABI_OK;
+}
+
 // ---------------------------------------------------------------- whole path from host buffers
 
 namespace {

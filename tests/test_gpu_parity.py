@@ -371,3 +371,40 @@ def test_c5_full_size_sampled(W, orc):
         u_o, _, _ = lut.hologram_window(pts, X0, Y0, B, B)
         u_g = field_np(pl.field[Y0:Y0 + B, X0:X0 + B])
         assert rel_l2(u_g, u_o) <= 1e-5
+
+
+# ---------------------------------------------------------------- conventional baseline (direct sum)
+def _direct_gpu(W, cfg, pts, row0, row1):
+    import torch
+    p = gpu_params(cfg)
+    pl = W.Pipeline(p, max(1, len(pts)), row0, row1)
+    d = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+    pl.build_tables()
+    pl.bin(d)
+    dense = torch.empty(W.psf_dense_bytes(p), dtype=torch.uint8, device="cuda")
+    W.build_psf_dense(p, dense)
+    u = torch.empty((row1 - row0, p.n_h, 2), dtype=torch.float32, device="cuda")
+    W.direct_sum(p, dense, pl.bins, row0, row1, u)
+    torch.cuda.synchronize()
+    return pl, field_np(u)
+
+
+@pytest.mark.parametrize("name,n,row0,row1,kw", [("C1", None, 0, 512, {}), ("C2", 3000, 512, 1024, {}),
+                                                 ("C1", 500, 128, 384, dict(tile=128, levels=6))])
+def test_direct_sum_equals_oracle_d2(W, orc, name, n, row0, row1, kw):
+    """GPU PSF stamping == the oracle's quantised direct sum D2 (Eq.(1) with snapped points/levels)."""
+    cfg = CONFIGS[name].replace(**kw)
+    pts = make_points(cfg, n=n)
+    _, u_g = _direct_gpu(W, cfg, pts, row0, row1)
+    P = orc_params(orc, cfg)
+    d2 = orc.direct_d2(P, pts.astype(np.float64), 0, row0, cfg.n_h, row1 - row0)
+    assert rel_l2(u_g, d2) <= 1e-5
+
+
+def test_wasabi_keep_all_aligned_equals_gpu_direct_sum(W):
+    """V3 between the two GPU paths: r=100%, aligned points -> WASABI u == direct sum (fp32)."""
+    cfg = CONFIGS["C2"].replace(retention=1.0, aligned=True, kind="levels", n_depth=8)
+    pts = make_points(cfg, n=400)
+    _, _, u_w, _ = _gpu_run(W, cfg, pts, 0, 2048)
+    _, u_d = _direct_gpu(W, cfg, pts, 0, 2048)
+    assert rel_l2(u_w, u_d) <= 1e-5
