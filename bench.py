@@ -167,19 +167,26 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
+    if args.same_device:        # test mode: every rank on cuda:0 (host logic check on a 1-GPU box)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -239,7 +246,7 @@ def run_ours(args, cfg):
     # checksum assembly after the timed region (the only collective: NCCL all_gather)
     cs = checksums(pl.field, pl.bits)
     if world > 1:
-        cs = gather_checksums(cs).sum(dim=0)
+        cs = gather_checksums(cs.to(cdev)).sum(dim=0)
     cs = cs.tolist()
 
     # roofline of the dominant kernel (algorithmic bytes per launch / event-timed duration)
@@ -325,6 +332,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="time the 4-call path (psi through HBM)")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo (test mode)")
+    ap.add_argument("--same-device", action="store_true", help="test mode: all ranks on cuda:0")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.points:
