@@ -109,7 +109,8 @@ wasabi_status wasabi_bin_points_bytes(const wasabi_params *params, int64_t n, in
 
 /* Step 2a: convert points to (ix, iy, iz) in fp64 (R-A3, R-A9, R-A17) and
  * build, for every T x T tile of band [row0, row1), the list of points (ascending index,
- * R-A11) whose footprint box [ix +- E] x [iy +- E] meets the tile.
+ * R-A11) whose footprint (R-A19: the kept coefficients' reach ek, q of the point's depth, see
+ * wasabi_export_reach) contains the tile.  The buffer bound uses the structural E >= ek.
  * d_points: n x 4 float32 (x, y, z, a) [m, m, m, -], 16-byte aligned, n >= 0.
  * d_bins: bin_bytes from wasabi_bin_points_bytes (or more); fully rewritten.
  * d_tables: built by wasabi_build_psf_tables with the same params. */
@@ -191,6 +192,14 @@ wasabi_status wasabi_tables_check(const wasabi_params *params, const void *d_tab
 wasabi_status wasabi_export_table(const wasabi_params *params, const void *d_tables, int32_t depth,
                                   int32_t *h_level, int32_t *h_dx, int32_t *h_dy, float *h_val, int64_t cap,
                                   int64_t *n_out);
+
+/* Export the footprint reach of one depth computed by the table build (reading R-A19): over the
+ * kept coefficients (level l, dX, dY) with h = 2^(l-1), *h_ek = max(max(|dX|, |dY|) + h) and
+ * *h_q = max((|dX| + h)^2 + (|dY| + h)^2).  Step 2a lists a point in a tile iff the tile meets
+ * [ix +- ek] x [iy +- ek] and its pixel nearest to (ix, iy) is within squared distance q.
+ * Synchronous device->host read. */
+wasabi_status wasabi_export_reach(const wasabi_params *params, const void *d_tables, int32_t depth, int32_t *h_ek,
+                                  int32_t *h_q);
 
 /* Export bins: h_tile_ptr (n_tiles + 1, tiles row-major within the band) and h_point_idx
  * (cap entries); *n_out = total entries (ENOSPC if cap is smaller). */

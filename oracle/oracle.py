@@ -86,11 +86,12 @@ def lib():
             L.orc_lut_build_depth.argtypes = [C.c_void_p, C.c_int]
             L.orc_lut_build_depth.restype = C.c_int64
             L.orc_points.argtypes = [_pp, _dp, C.c_int64, _i64p, _i64p, _i32p, _i8p]
-            L.orc_bins.argtypes = [_pp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, _i64p, _i32p,
-                                   C.c_int64]
+            L.orc_lut_reach.argtypes = [C.c_void_p, C.c_int, _i64p, _i64p]
+            L.orc_bins.argtypes = [_pp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p,
+                                   _i64p, _i32p, C.c_int64]
             L.orc_bins.restype = C.c_int64
-            L.orc_bin_tile.argtypes = [_pp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, _i32p,
-                                       C.c_int64]
+            L.orc_bin_tile.argtypes = [_pp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p,
+                                       _i32p, C.c_int64]
             L.orc_bin_tile.restype = C.c_int64
             L.orc_wasabi_window.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                             C.c_int64, _dp]
@@ -182,7 +183,36 @@ def points(P: Params, pts):
     return ix, iy, iz, ok.astype(bool)
 
 
+_reach_cache = {}
+
+
+def reach(P: Params):
+    """Per-depth footprint reach (ek, q) of the kept lists (orc_lut_reach, R-A19); cached per params."""
+    key = tuple(sorted(P.__dict__.items()))
+    if key not in _reach_cache:
+        lut = Lut(P)
+        ek = np.zeros(P.n_depth, np.int64)
+        q = np.zeros(P.n_depth, np.int64)
+        for d in range(P.n_depth):
+            a = np.zeros(1, np.int64); b = np.zeros(1, np.int64)
+            lib().orc_lut_reach(lut.h, d, _ptr(a, _i64p), _ptr(b, _i64p))
+            ek[d] = a[0]; q[d] = b[0]
+        lut.close()
+        _reach_cache[key] = (ek, q)
+    return _reach_cache[key]
+
+
+def reach_one(P: Params, d: int):
+    """(ek, q) of one depth (orc_lut_reach)."""
+    lut = Lut(P)
+    a = np.zeros(1, np.int64); b = np.zeros(1, np.int64)
+    lib().orc_lut_reach(lut.h, d, _ptr(a, _i64p), _ptr(b, _i64p))
+    lut.close()
+    return int(a[0]), int(b[0])
+
+
 def bins(P: Params, T: int, pts, row0: int, row1: int, cap: int = None):
+    ek, q = reach(P)
     p = _pts64(pts)
     n = p.shape[0]
     nt = (P.n_h // T) * ((row1 - row0) // T)
@@ -190,19 +220,21 @@ def bins(P: Params, T: int, pts, row0: int, row1: int, cap: int = None):
     cap = cap if cap is not None else max(1, n * 16)
     while True:
         idx = np.zeros(cap, np.int32)
-        tot = lib().orc_bins(C.byref(P.c()), T, _ptr(p, _dp), n, row0, row1, _ptr(ptr, _i64p),
-                             _ptr(idx, _i32p), cap)
+        tot = lib().orc_bins(C.byref(P.c()), T, _ptr(p, _dp), n, row0, row1, _ptr(ek, _i64p), _ptr(q, _i64p),
+                             _ptr(ptr, _i64p), _ptr(idx, _i32p), cap)
         if tot >= 0:
             return ptr, idx[:tot]
         cap = -tot
 
 
 def bin_tile(P: Params, T: int, pts, X0: int, Y0: int) -> np.ndarray:
+    ek, q = reach(P)
     p = _pts64(pts)
     n = p.shape[0]
     cap = max(1, n)
     idx = np.zeros(cap, np.int32)
-    tot = lib().orc_bin_tile(C.byref(P.c()), T, _ptr(p, _dp), n, X0, Y0, _ptr(idx, _i32p), cap)
+    tot = lib().orc_bin_tile(C.byref(P.c()), T, _ptr(p, _dp), n, X0, Y0, _ptr(ek, _i64p), _ptr(q, _i64p),
+                             _ptr(idx, _i32p), cap)
     return idx[:tot]
 
 

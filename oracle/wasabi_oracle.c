@@ -336,6 +336,26 @@ static orc_depth_list *orc_lut_get(orc_lut *t, int d) {
 /* Build (force) the list of depth d in the cache; returns N_r,d. */
 int64_t orc_lut_build_depth(void *h, int d) { return orc_lut_get((orc_lut *)h, d)->n; }
 
+/* Reach of depth d's kept list (reading R-A19).  A level-l entry (dX, dY) of a point at (ix, iy)
+ * lands at (s_l(ix) + dX, s_l(iy) + dY) (R-A8), and s_l(i) - i lies in (-2^(l-1), 2^(l-1)], so
+ * with h = 2^(l-1) the target is within |dX| + h of ix and |dY| + h of iy.  Over the kept list:
+ *   ek = max max(|dX|, |dY|) + h        (square bound)
+ *   q  = max (|dX| + h)^2 + (|dY| + h)^2  (squared-distance bound)
+ * The LL entries carry level L. */
+void orc_lut_reach(void *h, int d, int64_t *ek, int64_t *q) {
+    orc_depth_list *L = orc_lut_get((orc_lut *)h, d);
+    int64_t e = 0, qq = 0;
+    for (int64_t k = 0; k < L->n; k++) {
+        int64_t hl = (int64_t)1 << (L->level[k] - 1);
+        int64_t ax = llabs((long long)L->dx[k]) + hl, ay = llabs((long long)L->dy[k]) + hl;
+        if (ax > e) e = ax;
+        if (ay > e) e = ay;
+        if (ax * ax + ay * ay > qq) qq = ax * ax + ay * ay;
+    }
+    *ek = e;
+    *q = qq;
+}
+
 /* ---------------------------------------------------------------- points (step 2a) */
 
 /* R-A9 / R-A3 / R-A17: point -> (ix, iy, iz), valid flag.  pts is (n, 4) fp64 (x, y, z, a). */
@@ -370,27 +390,35 @@ int orc_points(const orc_params *P, const double *pts, int64_t n, int64_t *ix, i
 
 /* ---------------------------------------------------------------- bins (step 2a) */
 
+/* Footprint membership (R-A12, R-A19): tile [X0, X1] x [Y0, Y1] is in the footprint of a point at
+ * (ix, iy) of depth d iff it meets the square [ix - ek_d, ix + ek_d] x [iy - ek_d, iy + ek_d] and
+ * its pixel nearest to (ix, iy) lies within squared distance q_d (orc_lut_reach). */
+static int orc_tile_in_footprint(int64_t ix, int64_t iy, int64_t ek, int64_t q, int64_t X0, int64_t X1,
+                                 int64_t Y0, int64_t Y1) {
+    if (ix + ek < X0 || ix - ek > X1 || iy + ek < Y0 || iy - ek > Y1) return 0;
+    int64_t ddx = 0, ddy = 0;
+    if (ix < X0) ddx = X0 - ix;
+    if (ix > X1) ddx = ix - X1;
+    if (iy < Y0) ddy = Y0 - iy;
+    if (iy > Y1) ddy = iy - Y1;
+    return ddx * ddx + ddy * ddy <= q;
+}
+
 /* PAPER.md:115-122 sub-hologram re-basing, applied per T x T tile (R-A12): point j is in
- * bin(tx,ty) iff its footprint box [ix-E, ix+E] x [iy-E, iy+E] meets the tile and the tile
- * lies in rows [row0, row1).  Brute force over all tiles of the band, points ascending.
- * tile_ptr has n_tiles+1 entries (tiles row-major within the band).  Returns total entries,
- * or -(needed) if cap is too small (idx untouched beyond cap). */
+ * bin(tx,ty) iff the tile is in its footprint (orc_tile_in_footprint with the reach ek[iz], q[iz]
+ * of its depth) and lies in rows [row0, row1).  Brute force over all tiles of the band, points
+ * ascending.  tile_ptr has n_tiles+1 entries (tiles row-major within the band).  Returns total
+ * entries, or -(needed) if cap is too small (idx untouched beyond cap). */
 int64_t orc_bins(const orc_params *P, int64_t T, const double *pts, int64_t n, int64_t row0, int64_t row1,
-                 int64_t *tile_ptr, int32_t *idx, int64_t cap) {
+                 const int64_t *ek, const int64_t *q, int64_t *tile_ptr, int32_t *idx, int64_t cap) {
     int64_t tiles_x = P->n_h / T, tiles_y = (row1 - row0) / T;
-    double *Rz = (double *)malloc(sizeof(double) * (size_t)P->n_depth);
-    for (int d = 0; d < P->n_depth; d++) Rz[d] = orc_radius_px(P, orc_level_z(P, d));
-    int64_t half = (int64_t)1 << (P->levels - 1);
-    int64_t *bx = (int64_t *)malloc(sizeof(int64_t) * 4 * (size_t)(n > 0 ? n : 1));
+    int64_t *pp = (int64_t *)malloc(sizeof(int64_t) * 3 * (size_t)(n > 0 ? n : 1));
     int8_t *ok = (int8_t *)malloc((size_t)(n > 0 ? n : 1));
     for (int64_t j = 0; j < n; j++) {
         int64_t ix, iy;
         int iz;
         ok[j] = (int8_t)orc_point(P, pts + 4 * j, &ix, &iy, &iz);
-        if (!ok[j]) continue;
-        int64_t E = (int64_t)ceil(Rz[iz]) + 3 * half;
-        bx[4 * j + 0] = ix - E; bx[4 * j + 1] = ix + E;
-        bx[4 * j + 2] = iy - E; bx[4 * j + 3] = iy + E;
+        pp[3 * j + 0] = ix; pp[3 * j + 1] = iy; pp[3 * j + 2] = iz;
     }
     int64_t total = 0;
     for (int64_t ty = 0; ty < tiles_y; ty++)
@@ -400,28 +428,27 @@ int64_t orc_bins(const orc_params *P, int64_t T, const double *pts, int64_t n, i
             tile_ptr[t] = total;
             for (int64_t j = 0; j < n; j++) {
                 if (!ok[j]) continue;
-                if (bx[4 * j + 1] < X0 || bx[4 * j + 0] > X1) continue;
-                if (bx[4 * j + 3] < Y0 || bx[4 * j + 2] > Y1) continue;
+                int64_t d = pp[3 * j + 2];
+                if (!orc_tile_in_footprint(pp[3 * j], pp[3 * j + 1], ek[d], q[d], X0, X1, Y0, Y1)) continue;
                 if (total < cap) idx[total] = (int32_t)j;
                 total++;
             }
         }
     tile_ptr[tiles_x * tiles_y] = total;
-    free(ok); free(bx); free(Rz);
+    free(ok); free(pp);
     return total <= cap ? total : -total;
 }
 
-/* One bin by the same definition (for sampled parity at full size): points ascending whose box
- * meets tile [X0, X0+T) x [Y0, Y0+T) (absolute hologram rows).  Returns the count. */
+/* One bin by the same definition (for sampled parity at full size): points ascending whose
+ * footprint contains tile [X0, X0+T) x [Y0, Y0+T) (absolute hologram rows).  Returns the count. */
 int64_t orc_bin_tile(const orc_params *P, int64_t T, const double *pts, int64_t n, int64_t X0, int64_t Y0,
-                     int32_t *idx, int64_t cap) {
-    int64_t half = (int64_t)1 << (P->levels - 1), total = 0;
+                     const int64_t *ek, const int64_t *q, int32_t *idx, int64_t cap) {
+    int64_t total = 0;
     for (int64_t j = 0; j < n; j++) {
         int64_t ix, iy;
         int iz;
         if (!orc_point(P, pts + 4 * j, &ix, &iy, &iz)) continue;
-        int64_t E = (int64_t)ceil(orc_radius_px(P, orc_level_z(P, iz))) + 3 * half;
-        if (ix + E < X0 || ix - E > X0 + T - 1 || iy + E < Y0 || iy - E > Y0 + T - 1) continue;
+        if (!orc_tile_in_footprint(ix, iy, ek[iz], q[iz], X0, X0 + T - 1, Y0, Y0 + T - 1)) continue;
         if (total < cap) idx[total] = (int32_t)j;
         total++;
     }

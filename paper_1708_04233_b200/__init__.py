@@ -111,6 +111,7 @@ def lib() -> C.CDLL:
             "wasabi_tables_check": [_PP, _vp],
             "wasabi_export_table": [_PP, _vp, C.c_int32, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
             "wasabi_export_bins": [_PP, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
+            "wasabi_export_reach": [_PP, _vp, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
             "wasabi_bins_stats": [_vp, C.POINTER(_i64 * 8)],
         }
         for name, args in sig.items():
@@ -259,6 +260,14 @@ def export_table(p: Params, tables, depth: int):
     _check(lib().wasabi_export_table(C.byref(p.c()), _ptr(tables), depth, lv.ctypes.data, dx.ctypes.data,
                                      dy.ctypes.data, val.ctypes.data, cap, C.byref(n)))
     return lv[:n.value], dx[:n.value], dy[:n.value], val[:n.value, 0] + 1j * val[:n.value, 1].astype(np.complex64)
+
+
+def export_reach(p: Params, tables, depth: int):
+    """(ek, q) footprint reach of one depth as computed by the table build (R-A19)."""
+    ek = C.c_int32()
+    q = C.c_int32()
+    _check(lib().wasabi_export_reach(C.byref(p.c()), _ptr(tables), depth, C.byref(ek), C.byref(q)))
+    return ek.value, q.value
 
 
 def bins_stats(bins) -> dict:

@@ -21,7 +21,9 @@ __host__ __device__ inline uint32_t pack_entry_pos(int X, int Y, int level) {
 // Compact per-depth data read by the hot kernels (32 bytes).
 struct KDesc {
     int32_t H;                    // table half side
-    int32_t E;                    // footprint half-size (binning)
+    int32_t E;                    // structural footprint bound ceil(R) + 3 2^(L-1) (buffer sizing)
+    int32_t Ek;                   // kept reach, per axis (R-A19; computed by the table build)
+    int32_t Q;                    // kept reach, squared distance (R-A19; computed by the table build)
     int32_t ptr_base[kMaxLevels]; // level l (1..L) band pointer rows start at ptr_base[l-1]
 };
 

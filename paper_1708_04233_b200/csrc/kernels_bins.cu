@@ -45,13 +45,21 @@ __device__ __forceinline__ bool convert_point(const float4 p, const BinArgs &A, 
     return true;
 }
 
-// Tile range of a point's footprint box [ix-E, ix+E] x [iy-E, iy+E] within the band.
+// Tile range of a point's footprint square [ix-E, ix+E] x [iy-E, iy+E] within the band (E = Ek).
 __device__ __forceinline__ void tile_range(int ix, int iy, int E, const BinArgs &A, int &tx0, int &tx1, int &ty0,
                                            int &ty1) {
     tx0 = (int)max(0LL, floor_div((long long)ix - E, A.T));
     tx1 = (int)min((long long)A.tiles_x - 1, floor_div((long long)ix + E, A.T));
     ty0 = (int)max(0LL, floor_div((long long)iy - E - A.row0, A.T));
     ty1 = (int)min((long long)A.tiles_y - 1, floor_div((long long)iy + E - A.row0, A.T));
+}
+
+// Squared distance from coordinate i to the tile span [t0, t0 + T - 1] along one axis (0 inside).
+// With the square test of tile_range this is the footprint of R-A19: a tile is listed iff its
+// pixel nearest to (ix, iy) lies within squared distance Q of the point.
+__device__ __forceinline__ int sq_gap(int i, int t0, int T) {
+    const int g = i < t0 ? t0 - i : (i > t0 + T - 1 ? i - (t0 + T - 1) : 0);
+    return g * g;
 }
 
 __global__ void __launch_bounds__(256) convert_count_kernel(const float4 *__restrict__ pts, BinArgs A,
@@ -66,9 +74,14 @@ __global__ void __launch_bounds__(256) convert_count_kernel(const float4 *__rest
         pout[j] = make_int4(ix, iy, valid ? iz : -1, __float_as_int(p.w));
         if (valid) {
             int tx0, tx1, ty0, ty1;
-            tile_range(ix, iy, kd[iz].E, A, tx0, tx1, ty0, ty1);
-            for (int ty = ty0; ty <= ty1; ty++)
-                for (int tx = tx0; tx <= tx1; tx++) atomicAdd(&cnt[(int64_t)ty * A.tiles_x + tx], 1u);
+            const int Q = kd[iz].Q;
+            tile_range(ix, iy, kd[iz].Ek, A, tx0, tx1, ty0, ty1);
+            for (int ty = ty0; ty <= ty1; ty++) {
+                const int rem = Q - sq_gap(iy, (int)A.row0 + ty * A.T, A.T);
+                if (rem < 0) continue;
+                for (int tx = tx0; tx <= tx1; tx++)
+                    if (sq_gap(ix, tx * A.T, A.T) <= rem) atomicAdd(&cnt[(int64_t)ty * A.tiles_x + tx], 1u);
+            }
         }
     }
     const unsigned vb = __ballot_sync(0xffffffffu, valid);
@@ -88,13 +101,18 @@ __global__ void __launch_bounds__(256) scatter_kernel(BinArgs A, const KDesc *__
     const int4 q = pconv[j];
     if (q.z < 0) return;
     int tx0, tx1, ty0, ty1;
-    tile_range(q.x, q.y, kd[q.z].E, A, tx0, tx1, ty0, ty1);
-    for (int ty = ty0; ty <= ty1; ty++)
+    const int Q = kd[q.z].Q;
+    tile_range(q.x, q.y, kd[q.z].Ek, A, tx0, tx1, ty0, ty1);
+    for (int ty = ty0; ty <= ty1; ty++) {
+        const int rem = Q - sq_gap(q.y, (int)A.row0 + ty * A.T, A.T);
+        if (rem < 0) continue;
         for (int tx = tx0; tx <= tx1; tx++) {
+            if (sq_gap(q.x, tx * A.T, A.T) > rem) continue;
             const int64_t t = (int64_t)ty * A.tiles_x + tx;
             const uint32_t slot = atomicAdd(&fill[t], 1u);
             idx[ptr[t] + slot] = (uint32_t)j;
         }
+    }
 }
 
 // Warp-per-tile bitonic sort for bins of <= 1024 entries; larger bins are queued.

@@ -180,54 +180,73 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
                                                      int pass) {
     const TableHeader &h = hdr(tables);
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= h.total_ptrs) return;
-    const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
-    const KDesc *kd = at<KDesc>(tables, h.kdesc_off);
-    int32_t *ptr = atw<int32_t>(tables, h.ptr_off);
-    // depth: largest d with group_base <= g
-    int lo = 0, hi = n_depth;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (dd[mid].group_base <= g) lo = mid; else hi = mid;
-    }
-    const int d = lo;
-    const DDesc D = dd[d];
-    const KDesc K = kd[d];
-    int l = 1;
-    while (l < L && K.ptr_base[l] <= g) l++;
-    const int side = D.side;
-    const int nb = side >> l, hb = band_blocks(T, l);
-    const int64_t local = g - K.ptr_base[l - 1];
-    const int band = (int)(local / (nb + 1)), Xb = (int)(local % (nb + 1));
-    if (Xb == nb) {  // dummy slot: band end
-        if (pass == 0) ptr[g] = 0;
-        return;
-    }
-    const unsigned long long thr = st[d].prefix;
-    const int st_px = 1 << (l - 1);
-    const int yb1 = min(band * hb + hb, nb);
-    int out = pass ? ptr[g] : 0;
-    int cnt = 0;
-    uint4 *ent = atw<uint4>(tables, h.ent_off);
-    for (int Yb = band * hb; Yb < yb1; Yb++) {
-        for (int sb = (l == L ? 0 : 1); sb < 4; sb++) {
-            const int sbx = sb & 1, sby = sb >> 1;
-            const int X = (Xb << l) + sbx * st_px, Y = (Yb << l) + sby * st_px;
-            const uint32_t lin = (uint32_t)(Y * side + X);
-            const int64_t o = D.coef_off + (int64_t)Y * side + X;
-            const unsigned long long key = ((unsigned long long)coef_key[o] << 32) | (unsigned long long)(~lin);
-            if (key >= thr) {
-                if (pass) {
-                    const float2 v = coef_val[o];
-                    ent[out] = make_uint4(pack_entry_pos(X, Y, l), __float_as_uint(v.x), __float_as_uint(v.y), 0u);
-                    out++;
+    int d = 0, ek = 0, q = 0;      // this group's depth and kept reach (R-A19, pass 0)
+    if (g < h.total_ptrs) {
+        const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
+        const KDesc *kd = at<KDesc>(tables, h.kdesc_off);
+        int32_t *ptr = atw<int32_t>(tables, h.ptr_off);
+        // depth: largest d with group_base <= g
+        int lo = 0, hi = n_depth;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (dd[mid].group_base <= g) lo = mid; else hi = mid;
+        }
+        d = lo;
+        const DDesc D = dd[d];
+        const KDesc K = kd[d];
+        int l = 1;
+        while (l < L && K.ptr_base[l] <= g) l++;
+        const int side = D.side;
+        const int nb = side >> l, hb = band_blocks(T, l);
+        const int64_t local = g - K.ptr_base[l - 1];
+        const int band = (int)(local / (nb + 1)), Xb = (int)(local % (nb + 1));
+        if (Xb == nb) {  // dummy slot: band end
+            if (pass == 0) ptr[g] = 0;
+        } else {
+            const unsigned long long thr = st[d].prefix;
+            const int st_px = 1 << (l - 1);
+            const int yb1 = min(band * hb + hb, nb);
+            int out = pass ? ptr[g] : 0;
+            int cnt = 0;
+            uint4 *ent = atw<uint4>(tables, h.ent_off);
+            for (int Yb = band * hb; Yb < yb1; Yb++) {
+                for (int sb = (l == L ? 0 : 1); sb < 4; sb++) {
+                    const int sbx = sb & 1, sby = sb >> 1;
+                    const int X = (Xb << l) + sbx * st_px, Y = (Yb << l) + sby * st_px;
+                    const uint32_t lin = (uint32_t)(Y * side + X);
+                    const int64_t o = D.coef_off + (int64_t)Y * side + X;
+                    const unsigned long long key = ((unsigned long long)coef_key[o] << 32) | (unsigned long long)(~lin);
+                    if (key >= thr) {
+                        if (pass) {
+                            const float2 v = coef_val[o];
+                            ent[out] = make_uint4(pack_entry_pos(X, Y, l), __float_as_uint(v.x), __float_as_uint(v.y), 0u);
+                            out++;
+                        } else {
+                            // target within |dX| + 2^(l-1) of the point per axis (s_l(i) - i in (-h, h])
+                            const int ax = abs(X - K.H) + st_px, ay = abs(Y - K.H) + st_px;
+                            ek = max(ek, max(ax, ay));
+                            q = max(q, ax * ax + ay * ay);
+                        }
+                        cnt++;
+                    }
                 }
-                cnt++;
             }
+            if (pass == 0) ptr[g] = cnt;
         }
     }
-    (void)K;
-    if (pass == 0) ptr[g] = cnt;
+    if (pass == 0) {
+        // per-depth max of the reach: one atomic per warp when the warp is within one depth
+        KDesc *kdw = atw<KDesc>(tables, h.kdesc_off);
+        const int dmin = __reduce_min_sync(0xffffffffu, d), dmax = __reduce_max_sync(0xffffffffu, d);
+        if (dmin == dmax) {
+            ek = __reduce_max_sync(0xffffffffu, ek);
+            q = __reduce_max_sync(0xffffffffu, q);
+            if ((threadIdx.x & 31) == 0 && q > 0) { atomicMax(&kdw[d].Ek, ek); atomicMax(&kdw[d].Q, q); }
+        } else if (q > 0) {
+            atomicMax(&kdw[d].Ek, ek);
+            atomicMax(&kdw[d].Q, q);
+        }
+    }
 }
 
 }  // namespace

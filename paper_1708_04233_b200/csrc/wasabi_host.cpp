@@ -566,6 +566,23 @@ wasabi_status wasabi_tables_check(const wasabi_params *params, const void *d_tab
     return WASABI_OK;
 }
 
+wasabi_status wasabi_export_reach(const wasabi_params *params, const void *d_tables, int32_t depth, int32_t *h_ek,
+                                  int32_t *h_q) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if ((st = wasabi_tables_check(params, d_tables)) != WASABI_OK) return st;
+    if (depth < 0 || depth >= g.nd) return fail(WASABI_EINVAL, "depth out of range");
+    if (!h_ek || !h_q) return fail(WASABI_EINVAL, "null output");
+    KDesc K;
+    CK(cudaMemcpy(&K, static_cast<const char *>(d_tables) + g.th.kdesc_off + sizeof(KDesc) * (size_t)depth,
+                  sizeof K, cudaMemcpyDeviceToHost),
+       "read kdesc");
+    *h_ek = K.Ek;
+    *h_q = K.Q;
+    return WASABI_OK;
+}
+
 wasabi_status wasabi_export_table(const wasabi_params *params, const void *d_tables, int32_t depth, int32_t *h_level,
                                   int32_t *h_dx, int32_t *h_dy, float *h_val, int64_t cap, int64_t *n_out) {
     Geo g;

@@ -41,6 +41,7 @@ def _compare_depth(W, orc, p, P, t, d):
     assert np.array_equal(lv, olv) and np.array_equal(dx, odx) and np.array_equal(dy, ody), f"depth {d}"
     scale = np.max(np.abs(oval))
     assert np.max(np.abs(val - oval)) <= 1e-6 * scale + 1e-7, f"depth {d} values"
+    assert W.export_reach(p, t, d) == orc.reach_one(P, d), f"depth {d} reach (R-A19)"
 
 
 # ---------------------------------------------------------------- step 1: tables (bit-exact indices)

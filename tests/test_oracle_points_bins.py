@@ -64,18 +64,23 @@ def test_paper_subhologram_rebasing_example(orc):
 
 
 def _numpy_bins(orc, P, T, pts, row0, row1):
+    """Tile lists by the footprint definition (R-A12, R-A19), enumerated with numpy per point."""
     ix, iy, iz, ok = orc.points(P, pts)
-    geo = orc.geometry(P)
-    E = geo["E"][iz]
+    ek_d, q_d = orc.reach(P)
     tx_n = P.n_h // T
     ty_n = (row1 - row0) // T
     lists = [[] for _ in range(tx_n * ty_n)]
+    X0 = np.arange(tx_n) * T
+    Y0 = row0 + np.arange(ty_n) * T
     for j in np.flatnonzero(ok):
-        x0 = max(0, (ix[j] - E[j]) // T); x1 = min(tx_n - 1, (ix[j] + E[j]) // T)
-        y0 = max(0, (iy[j] - E[j] - row0) // T); y1 = min(ty_n - 1, (iy[j] + E[j] - row0) // T)
-        for ty in range(int(y0), int(y1) + 1):
-            for tx in range(int(x0), int(x1) + 1):
-                lists[ty * tx_n + tx].append(j)
+        ek, q = ek_d[iz[j]], q_d[iz[j]]
+        ddx = np.maximum(np.maximum(X0 - ix[j], ix[j] - (X0 + T - 1)), 0)
+        ddy = np.maximum(np.maximum(Y0 - iy[j], iy[j] - (Y0 + T - 1)), 0)
+        mx = ddx <= ek
+        my = ddy <= ek
+        member = my[:, None] & mx[None, :] & (ddy[:, None] ** 2 + ddx[None, :] ** 2 <= q)
+        for t in np.flatnonzero(member.reshape(-1)):
+            lists[t].append(j)
     ptr = np.zeros(len(lists) + 1, np.int64)
     ptr[1:] = np.cumsum([len(l) for l in lists])
     idx = np.array([j for l in lists for j in l], np.int32)
@@ -83,9 +88,9 @@ def _numpy_bins(orc, P, T, pts, row0, row1):
 
 
 @pytest.mark.parametrize("row0,row1", [(0, 512), (128, 320)])
-def test_bins_equal_numpy_box_enumeration(orc, row0, row1):
-    """Every valid point appears, in ascending order, in exactly the tiles its footprint box
-    [ix +- E] x [iy +- E] touches (E = ceil(R) + 3 2^(L-1)), restricted to the band."""
+def test_bins_equal_numpy_footprint_enumeration(orc, row0, row1):
+    """Every valid point appears, in ascending order, in exactly the tiles of its footprint
+    (square +- ek_d and squared distance <= q_d, R-A19), restricted to the band."""
     c = CONFIGS["C1"]
     P = orc.Params.from_config(c)
     pts = make_points(c, n=300)
@@ -106,15 +111,56 @@ def test_bins_equal_numpy_box_enumeration(orc, row0, row1):
         assert np.array_equal(orc.bin_tile(P, 64, pts, X0, Y0), idx[ptr[t]:ptr[t + 1]])
 
 
-def test_footprint_box_covers_every_retained_coefficient(orc):
-    """E_d bounds |target - ix| for every retained coefficient of every level (R-A8 shift
-    included), so a point outside a tile's box cannot contribute to it."""
+@pytest.mark.parametrize("retention", [0.05, 1.0])
+def test_reach_covers_every_retained_coefficient(orc, retention):
+    """R-A19: for every depth and every sub-position of the point on the 2^L grid, every retained
+    coefficient of every level lands within ek_d (per axis) and within squared distance q_d of the
+    point (R-A8 shift included); the bound is tight to one pixel; ek_d <= the structural E_d."""
     c = CONFIGS["C1"]
-    P = orc.Params.from_config(c).__class__(**{**orc.Params.from_config(c).__dict__, "retention": 1.0})
+    P = orc.Params(**{**orc.Params.from_config(c).__dict__, "retention": retention})
     geo = orc.geometry(P)
+    ek_d, q_d = orc.reach(P)
     for d in range(P.n_depth):
         lv, dx, dy, _ = orc.select(P, d, int(geo["n_r"][d]))
+        worst_ax, worst_q = 0, 0
         for rho in range(1 << P.levels):
-            ix = 1000 + rho
-            s = np.array([(1 << l) * ((ix + (1 << (l - 1))) >> l) for l in lv])
-            assert np.max(np.abs(s + dx - ix)) <= geo["E"][d]
+            i = 1000 + rho
+            s = np.array([(1 << l) * ((i + (1 << (l - 1))) >> l) for l in lv])
+            tx = np.abs(s + dx - i)
+            ty = np.abs(s + dy - i)          # same sub-position on both axes
+            worst_ax = max(worst_ax, int(tx.max()), int(ty.max()))
+            worst_q = max(worst_q, int((tx * tx + ty * ty).max()))
+            assert tx.max() <= ek_d[d] and ty.max() <= ek_d[d]
+            assert (tx * tx + ty * ty).max() <= q_d[d]
+        assert ek_d[d] - worst_ax <= 1
+        assert ek_d[d] <= geo["E"][d]
+        assert q_d[d] >= worst_q
+
+
+def test_bins_contain_every_tile_a_point_writes(orc):
+    """Brute force through Eq.(2) itself: for single points at assorted sub-pixel grid positions and
+    depths, every tile holding a nonzero psi coefficient of that point (oracle WASABI window over the
+    whole hologram) lists the point; and the footprint is much smaller than the old 3 2^(L-1) box."""
+    c = CONFIGS["C1"]
+    P = orc.Params.from_config(c)
+    lut = orc.Lut(P)
+    T = 64
+    n_h = P.n_h
+    rng = np.random.default_rng(7)
+    for trial in range(6):
+        ix, iy = int(rng.integers(0, n_h)), int(rng.integers(0, n_h))
+        d = int(rng.integers(0, P.n_depth))
+        dz = (P.z_max - P.z_min) / (P.n_depth - 1)
+        pt = np.array([[(ix - n_h // 2) * P.pitch, (iy - n_h // 2) * P.pitch, P.z_min + d * dz, 1.0]])
+        psi, cnt = lut.wasabi_window(pt, 0, 0, n_h, n_h)
+        assert cnt > 0
+        ys, xs = np.nonzero(psi)
+        written = set(((ys // T) * (n_h // T) + xs // T).tolist())
+        ptr, idx = orc.bins(P, T, pt, 0, n_h)
+        listed = {t for t in range(len(ptr) - 1) if ptr[t + 1] > ptr[t]}
+        assert written <= listed
+        E = int(orc.geometry(P)["E"][d])
+        bx = range(max(0, (ix - E) // T), min(n_h // T - 1, (ix + E) // T) + 1)
+        by = range(max(0, (iy - E) // T), min(n_h // T - 1, (iy + E) // T) + 1)
+        assert len(listed) <= len(bx) * len(by)
+    lut.close()
