@@ -15,7 +15,8 @@
 //            all targets of a chunk are distinct: no atomics, no races).  The current point's range
 //            prefixes live in registers (lane r holds range r); lane -> range uses one REDUX.OR
 //            marker + two POPCs; a kD-deep register ring prefetches the entry loads.
-// LUT entries are 16-byte records (X | Y << 14 | level << 28, re, im): target = Y*S + X + base.
+// LUT entries are 16-byte records (pos = X | Y << 14 | level << 28, re, im, Y*S + X - pos):
+// target = pos + word3 + base (one IADD3; every word of the 128-bit load is used).
 // Rows outside the tile (band rounding) are rejected by one unsigned compare of the smem address
 // (X ranges are exact).  psi is written once, coalesced.  Per-pixel accumulation order is fixed
 // (point order): bitwise deterministic and independent of the band split.
@@ -34,7 +35,7 @@ struct SupArgs {
 };
 
 constexpr int kPB = 8;                 // points per range batch
-constexpr int kD = 8;                  // prefetch depth (chunks)
+constexpr int kD = 4;                  // prefetch depth (chunks)
 constexpr int kEmpty = 0x3fffffff;
 constexpr int kBadBase = 0x3fffffff;   // base of padding lanes: address always >= T*S
 
@@ -206,11 +207,11 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
     if (np > 0) { totp = tot_s[0]; exv = lane < SEGW ? ex_s[0][lane] : kEmpty; ap = a_s[0]; }
     bool done = np == 0;
 
-    uint32_t rw[kD];
+    uint32_t rw[kD], rz[kD];
     float rx[kD], ry[kD], ra[kD];
     int rb[kD];
 #pragma unroll
-    for (int s = 0; s < kD; s++) { rw[s] = 0; rx[s] = 0.f; ry[s] = 0.f; ra[s] = 0.f; }
+    for (int s = 0; s < kD; s++) { rw[s] = 0; rz[s] = 0; rx[s] = 0.f; ry[s] = 0.f; ra[s] = 0.f; }
 #define WASABI_PREFETCH(s)                                                                  \
     do {                                                                                    \
         rb[s] = kBadBase;                                                                   \
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
             const int2 d = rec_s[kp][rr & (SEGW - 1)];                                      \
             if (e < totp) {                                                                 \
                 const uint4 en = __ldg(tent + e + d.x);                                     \
-                rw[s] = en.x; rx[s] = __uint_as_float(en.y); ry[s] = __uint_as_float(en.z); \
+                rw[s] = en.x; rx[s] = __uint_as_float(en.y); ry[s] = __uint_as_float(en.z); rz[s] = en.w; \
                 rb[s] = d.y; ra[s] = ap;                                                    \
             }                                                                               \
             cp += 32;                                                                       \
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
     } while (0)
 #define WASABI_CONSUME(s)                                                                   \
     do {                                                                                    \
-        const int addr = (int)((rw[s] >> 14) & 0x3fffu) * S + (int)(rw[s] & 0x3fffu) + rb[s]; \
+        const int addr = (int)(rw[s] + rz[s]) + rb[s];                                       \
         const uint32_t sa = (unsigned)(addr - sub_lo) < (unsigned)(Th * S)                  \
                                 ? tile_sa + 8u * (uint32_t)addr : dummy_sa;                 \
         float2 o = lds2(sa);                                                                \

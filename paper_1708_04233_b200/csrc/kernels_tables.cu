@@ -219,7 +219,13 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
                     if (key >= thr) {
                         if (pass) {
                             const float2 v = coef_val[o];
-                            ent[out] = make_uint4(pack_entry_pos(X, Y, l), __float_as_uint(v.x), __float_as_uint(v.y), 0u);
+                            // word 3 = (Y*S + X) - pos (mod 2^32): the superpose kernel forms the
+                            // shared-memory offset as pos + word3 + base in one add, and no word of
+                            // the 128-bit load is dead (a dead word is a write-after-write hazard
+                            // on the in-flight load once its register is reused)
+                            const uint32_t pos = pack_entry_pos(X, Y, l);
+                            const uint32_t off = (uint32_t)(Y * (T + 1) + X);
+                            ent[out] = make_uint4(pos, __float_as_uint(v.x), __float_as_uint(v.y), off - pos);
                             out++;
                         } else {
                             // target within |dX| + 2^(l-1) of the point per axis (s_l(i) - i in (-h, h])

@@ -5,6 +5,9 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+for i, arg in enumerate(sys.argv):          # --pkg DIR: import the package from a variant copy
+    if arg == "--pkg":
+        sys.path.insert(0, os.path.abspath(sys.argv[i + 1]))
 import torch  # noqa: E402
 
 import paper_1708_04233_b200 as W  # noqa: E402
@@ -16,6 +19,7 @@ ap.add_argument("--row0", type=int, default=32768)
 ap.add_argument("--rows", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tile", type=int, default=None)
+ap.add_argument("--pkg", default=None)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 if a.tile:
@@ -33,4 +37,4 @@ for _ in range(a.reps):
 ev[1].record()
 torch.cuda.synchronize()
 st = W.bins_stats(pl.bins)
-print(f"superpose {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
+print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} superpose {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
