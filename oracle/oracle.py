@@ -35,7 +35,7 @@ def build(force: bool = False) -> str:
 class _Params(C.Structure):
     _fields_ = [("wavelength", C.c_double), ("pitch", C.c_double), ("n_h", C.c_int64),
                 ("n_depth", C.c_int32), ("levels", C.c_int32), ("z_min", C.c_double),
-                ("z_max", C.c_double), ("retention", C.c_double)]
+                ("z_max", C.c_double), ("retention", C.c_double), ("exact", C.c_int32), ("pad", C.c_int32)]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -48,15 +48,27 @@ class Params:
     z_min: float
     z_max: float
     retention: float
+    exact: bool = False      # R-A20 offset-class tables
 
     @staticmethod
-    def from_config(cfg) -> "Params":
+    def from_config(cfg, exact: bool = False) -> "Params":
         return Params(cfg.wavelength, cfg.pitch, cfg.n_h, cfg.n_depth, cfg.levels, cfg.z_min,
-                      cfg.z_max, cfg.retention)
+                      cfg.z_max, cfg.retention, exact)
+
+    @property
+    def n_tables(self) -> int:
+        return self.n_depth << (2 * self.levels) if self.exact else self.n_depth
+
+    def table_index(self, ix, iy, iz):
+        """Table of a point (R-A20): iz, or iz 4^L + (iy mod 2^L) 2^L + (ix mod 2^L) in exact mode."""
+        if not self.exact:
+            return iz
+        m = (1 << self.levels) - 1
+        return (np.asarray(iz, np.int64) << (2 * self.levels)) | ((np.asarray(iy) & m) << self.levels) | (np.asarray(ix) & m)
 
     def c(self) -> _Params:
         return _Params(self.wavelength, self.pitch, self.n_h, self.n_depth, self.levels, self.z_min,
-                       self.z_max, self.retention)
+                       self.z_max, self.retention, int(self.exact), 0)
 
 
 _dp = C.POINTER(C.c_double)
@@ -74,19 +86,22 @@ def lib():
             L = C.CDLL(build())
             L.orc_geometry.argtypes = [_pp, _dp, _dp, _i64p, _i64p, _i64p, _i64p]
             L.orc_depth_info.argtypes = [_pp, C.c_int, _dp, _i64p]
-            L.orc_psf_table.argtypes = [_pp, C.c_int, _dp]
+            L.orc_psf_table.argtypes = [_pp, C.c_int64, _dp]
             L.orc_haar_fwd.argtypes = [_dp, C.c_int64, C.c_int64, C.c_int64, C.c_int]
             L.orc_haar_inv.argtypes = [_dp, C.c_int64, C.c_int64, C.c_int64, C.c_int]
-            L.orc_table_coeffs.argtypes = [_pp, C.c_int, _dp]
-            L.orc_select.argtypes = [_pp, C.c_int, _i32p, _i32p, _i32p, _dp, C.c_int64]
+            L.orc_table_coeffs.argtypes = [_pp, C.c_int64, _dp]
+            L.orc_select.argtypes = [_pp, C.c_int64, _i32p, _i32p, _i32p, _dp, C.c_int64]
+            L.orc_table_info.argtypes = [_pp, C.c_int64, _i64p]
+            L.orc_n_tables.argtypes = [_pp]
+            L.orc_n_tables.restype = C.c_int64
             L.orc_select.restype = C.c_int64
             L.orc_lut_new.argtypes = [_pp]
             L.orc_lut_new.restype = C.c_void_p
             L.orc_lut_free.argtypes = [C.c_void_p]
-            L.orc_lut_build_depth.argtypes = [C.c_void_p, C.c_int]
+            L.orc_lut_build_depth.argtypes = [C.c_void_p, C.c_int64]
             L.orc_lut_build_depth.restype = C.c_int64
             L.orc_points.argtypes = [_pp, _dp, C.c_int64, _i64p, _i64p, _i32p, _i8p]
-            L.orc_lut_reach.argtypes = [C.c_void_p, C.c_int, _i64p, _i64p]
+            L.orc_lut_reach.argtypes = [C.c_void_p, C.c_int64, _i64p, _i64p]
             L.orc_bins.argtypes = [_pp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p,
                                    _i64p, _i32p, C.c_int64]
             L.orc_bins.restype = C.c_int64
@@ -129,9 +144,16 @@ def geometry(P: Params) -> dict:
     return dict(z=z, R=R, H=H, E=E, nnz=nnz, n_r=nr)
 
 
+def table_info(P: Params, t: int) -> dict:
+    """Table t (R-A20): H (aligned centre), side, structural nnz, N_r."""
+    h = np.zeros(4, np.int64)
+    lib().orc_table_info(C.byref(P.c()), int(t), _ptr(h, _i64p))
+    return dict(H=int(h[0]), side=int(h[1]), nnz=int(h[2]), n_r=int(h[3]))
+
+
 def psf_table(P: Params, d: int) -> np.ndarray:
-    H = int(geometry_one(P, d)["H"])
-    f = np.zeros((2 * H, 2 * H, 2))
+    side = table_info(P, d)["side"]
+    f = np.zeros((side, side, 2))
     lib().orc_psf_table(C.byref(P.c()), d, _ptr(f, _dp))
     return f[..., 0] + 1j * f[..., 1]
 
@@ -157,8 +179,9 @@ def haar_inv(f: np.ndarray, L: int) -> np.ndarray:
     return b[..., 0] + 1j * b[..., 1]
 
 
-def table_coeffs(P: Params, d: int, H: int) -> np.ndarray:
-    c = np.zeros((2 * H, 2 * H, 2))
+def table_coeffs(P: Params, d: int, H: int = None) -> np.ndarray:
+    side = table_info(P, d)["side"]
+    c = np.zeros((side, side, 2))
     lib().orc_table_coeffs(C.byref(P.c()), d, _ptr(c, _dp))
     return c[..., 0] + 1j * c[..., 1]
 
@@ -191,9 +214,9 @@ def reach(P: Params):
     key = tuple(sorted(P.__dict__.items()))
     if key not in _reach_cache:
         lut = Lut(P)
-        ek = np.zeros(P.n_depth, np.int64)
-        q = np.zeros(P.n_depth, np.int64)
-        for d in range(P.n_depth):
+        ek = np.zeros(P.n_tables, np.int64)
+        q = np.zeros(P.n_tables, np.int64)
+        for d in range(P.n_tables):
             a = np.zeros(1, np.int64); b = np.zeros(1, np.int64)
             lib().orc_lut_reach(lut.h, d, _ptr(a, _i64p), _ptr(b, _i64p))
             ek[d] = a[0]; q[d] = b[0]

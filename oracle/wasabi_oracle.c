@@ -43,7 +43,22 @@ typedef struct {
     int32_t levels;      /* L, wavelet levels (Haar here) */
     double z_min, z_max; /* depth range [m] */
     double retention;    /* r in (0,1] (north_star "top-r%") */
+    int32_t exact;       /* 1: exact off-grid shifts via offset-class tables */
+    int32_t pad;
 } orc_params;
+
+/* R-A20 (NEXT-4): with exact = 1 every depth has 4^L tables, one per sub-position class
+ * (cx, cy) = (ix mod 2^L, iy mod 2^L); table t = d 4^L + cy 2^L + cx holds the PSF centred at
+ * (H + cx, H + cy) in a (2H + 2^L)^2 table, and a point's coefficients of every level are shifted
+ * by the 2^L-aligned s = (ix - cx, iy - cy), so WASABI at r = 100% equals the quantised direct sum
+ * for any integer position.  exact = 0: one table per depth (t = d), centre (H, H), side 2H. */
+static int orc_cls_bits(const orc_params *P) { return P->exact ? P->levels : 0; }
+int64_t orc_n_tables(const orc_params *P) { return (int64_t)P->n_depth << (2 * orc_cls_bits(P)); }
+static int orc_table_depth(const orc_params *P, int64_t t) { return (int)(t >> (2 * orc_cls_bits(P))); }
+static int64_t orc_table_cx(const orc_params *P, int64_t t) { return t & (((int64_t)1 << orc_cls_bits(P)) - 1); }
+static int64_t orc_table_cy(const orc_params *P, int64_t t) {
+    return (t >> orc_cls_bits(P)) & (((int64_t)1 << orc_cls_bits(P)) - 1);
+}
 
 /* ---------------------------------------------------------------- geometry */
 
@@ -80,11 +95,11 @@ static int orc_in_support(int64_t dx, int64_t dy, double R) {
 /* Structural nnz_d (R-A4): number of coefficient positions whose support block touches S_d.
  * Brute force over the mask: level-l detail coefficients (3 per 2^l block) and level-L
  * scaling coefficients (1 per 2^L block). */
-static int64_t orc_nnz(const orc_params *P, int64_t H, double R) {
-    int64_t side = 2 * H, nnz = 0;
+static int64_t orc_nnz_c(const orc_params *P, int64_t side, int64_t Cx, int64_t Cy, double R) {
+    int64_t nnz = 0;
     unsigned char *m = (unsigned char *)calloc((size_t)(side * side), 1);
     for (int64_t Y = 0; Y < side; Y++)
-        for (int64_t X = 0; X < side; X++) m[Y * side + X] = (unsigned char)orc_in_support(X - H, Y - H, R);
+        for (int64_t X = 0; X < side; X++) m[Y * side + X] = (unsigned char)orc_in_support(X - Cx, Y - Cy, R);
     for (int l = 1; l <= P->levels; l++) {
         int64_t b = (int64_t)1 << l;
         for (int64_t Y0 = 0; Y0 < side; Y0 += b)
@@ -99,12 +114,34 @@ static int64_t orc_nnz(const orc_params *P, int64_t H, double R) {
     free(m);
     return nnz;
 }
+static int64_t orc_nnz(const orc_params *P, int64_t H, double R) { return orc_nnz_c(P, 2 * H, H, H, R); }
+
+/* Table t geometry (R-A20): depth, H, side, PSF centre (Cx, Cy). */
+static void orc_table_geom(const orc_params *P, int64_t t, int *d, double *R, int64_t *H, int64_t *side,
+                           int64_t *Cx, int64_t *Cy) {
+    *d = orc_table_depth(P, t);
+    *R = orc_radius_px(P, orc_level_z(P, *d));
+    *H = orc_half(P, *R);
+    *side = 2 * *H + (P->exact ? ((int64_t)1 << P->levels) : 0);
+    *Cx = *H + orc_table_cx(P, t);
+    *Cy = *H + orc_table_cy(P, t);
+}
+
 
 /* R-A4: N_r,d = min(nnz, ceil(r_ppm * nnz / 1e6)), r_ppm = llround(r * 1e6). */
 static int64_t orc_n_r(const orc_params *P, int64_t nnz) {
     int64_t r_ppm = llround(P->retention * 1e6);
     int64_t n = (r_ppm * nnz + 999999) / 1000000;
     return n < nnz ? n : nnz;
+}
+
+/* Geometry of table t: hsn = {H, side, nnz, N_r}. */
+int orc_table_info(const orc_params *P, int64_t t, int64_t *hsn) {
+    int d; double R; int64_t H, side, Cx, Cy;
+    orc_table_geom(P, t, &d, &R, &H, &side, &Cx, &Cy);
+    int64_t c = orc_nnz_c(P, side, Cx, Cy, R);
+    hsn[0] = H; hsn[1] = side; hsn[2] = c; hsn[3] = orc_n_r(P, c);
+    return 0;
 }
 
 /* Per-depth geometry.  E_d = ceil(R_d) + 3*2^(L-1) is the footprint half-size (bins). */
@@ -140,14 +177,15 @@ int orc_depth_info(const orc_params *P, int d, double *zr, int64_t *hen) {
 /* ---------------------------------------------------------------- PSF (step 1) */
 
 /* u_z = exp(i k r) circ(.), unit amplitude (Eq.(1) carries only a_j).
- * Table of side 2H, centre at (H, H); f is interleaved (re, im) row-major. */
-int orc_psf_table(const orc_params *P, int d, double *f) {
-    double z = orc_level_z(P, d), R = orc_radius_px(P, z);
-    int64_t H = orc_half(P, R), side = 2 * H;
+ * Table t (R-A20): side 2H (+ 2^L in exact mode), centre (Cx, Cy); f interleaved (re, im) row-major. */
+int orc_psf_table(const orc_params *P, int64_t t, double *f) {
+    int d; double R; int64_t H, side, Cx, Cy;
+    orc_table_geom(P, t, &d, &R, &H, &side, &Cx, &Cy);
+    double z = orc_level_z(P, d);
     double k = 2.0 * ORC_PI / P->wavelength;
     for (int64_t Y = 0; Y < side; Y++)
         for (int64_t X = 0; X < side; X++) {
-            int64_t dx = X - H, dy = Y - H;
+            int64_t dx = X - Cx, dy = Y - Cy;
             double *o = f + 2 * (Y * side + X);
             if (!orc_in_support(dx, dy, R)) { o[0] = 0.0; o[1] = 0.0; continue; }
             double xp = (double)dx * P->pitch, yp = (double)dy * P->pitch;
@@ -235,26 +273,28 @@ static int orc_canon_cmp(const void *a, const void *b) {
 }
 
 /* Full transformed table of depth d (for invariant tests).  coef: (2H)^2 interleaved complex. */
-int orc_table_coeffs(const orc_params *P, int d, double *coef) {
-    orc_psf_table(P, d, coef);
-    double R = orc_radius_px(P, orc_level_z(P, d));
-    int64_t side = 2 * orc_half(P, R);
+int orc_table_coeffs(const orc_params *P, int64_t t, double *coef) {
+    int d; double R; int64_t H, side, Cx, Cy;
+    orc_table_geom(P, t, &d, &R, &H, &side, &Cx, &Cy);
+    orc_psf_table(P, t, coef);
     orc_haar_fwd(coef, side, side, side, P->levels);
     return 0;
 }
 
 /* PAPER.md:92 "select N_r strong coefficients among the wavelet-domain PSF and store them in
- * the LUT".  Full sort of all (2H)^2 positions by (kappa desc, linear index asc) (R-A13, R-A5),
- * first N_r kept, then re-sorted canonically by (level, Y, X).  Outputs level, dx = X - H,
- * dy = Y - H, fp64 value (re, im).  Returns the count (N_r,d) or -1 if cap is too small. */
-int64_t orc_select(const orc_params *P, int d, int32_t *level, int32_t *dx, int32_t *dy, double *val,
+ * the LUT".  Full sort of all side^2 positions of table t by (kappa desc, linear index asc)
+ * (R-A13, R-A5), first N_r kept, then re-sorted canonically by (level, Y, X).  Outputs level,
+ * dx = X - H, dy = Y - H (offsets from the 2^L-aligned table centre (H, H)), fp64 value (re, im).
+ * Returns the count (N_r) or -1 if cap is too small. */
+int64_t orc_select(const orc_params *P, int64_t t, int32_t *level, int32_t *dx, int32_t *dy, double *val,
                    int64_t cap) {
-    double z = orc_level_z(P, d), R = orc_radius_px(P, z);
-    int64_t H = orc_half(P, R), side = 2 * H, n = side * side;
-    int64_t nr = orc_n_r(P, orc_nnz(P, H, R));
+    int d; double R; int64_t H, side, Cx, Cy;
+    orc_table_geom(P, t, &d, &R, &H, &side, &Cx, &Cy);
+    int64_t n = side * side;
+    int64_t nr = orc_n_r(P, orc_nnz_c(P, side, Cx, Cy, R));
     if (nr > cap) return -1;
     double *c = (double *)malloc(sizeof(double) * 2 * (size_t)n);
-    orc_table_coeffs(P, d, c);
+    orc_table_coeffs(P, t, c);
     orc_key *keys = (orc_key *)malloc(sizeof(orc_key) * (size_t)n);
     for (int64_t i = 0; i < n; i++) {
         double re = c[2 * i], im = c[2 * i + 1];
@@ -303,27 +343,27 @@ typedef struct {
 void *orc_lut_new(const orc_params *P) {
     orc_lut *t = (orc_lut *)calloc(1, sizeof(orc_lut));
     t->P = *P;
-    t->lists = (orc_depth_list *)calloc((size_t)P->n_depth, sizeof(orc_depth_list));
+    t->lists = (orc_depth_list *)calloc((size_t)orc_n_tables(P), sizeof(orc_depth_list));
     return t;
 }
 
 void orc_lut_free(void *h) {
     orc_lut *t = (orc_lut *)h;
     if (!t) return;
-    for (int d = 0; d < t->P.n_depth; d++) {
+    for (int64_t d = 0; d < orc_n_tables(&t->P); d++) {
         free(t->lists[d].level); free(t->lists[d].dx); free(t->lists[d].dy); free(t->lists[d].val);
     }
     free(t->lists);
     free(t);
 }
 
-static orc_depth_list *orc_lut_get(orc_lut *t, int d) {
+static orc_depth_list *orc_lut_get(orc_lut *t, int64_t d) {
     orc_depth_list *L = &t->lists[d];
     if (L->built) return L;
     const orc_params *P = &t->P;
-    double R = orc_radius_px(P, orc_level_z(P, d));
-    L->H = orc_half(P, R);
-    int64_t cap = orc_n_r(P, orc_nnz(P, L->H, R));
+    int dd; double R; int64_t side, Cx, Cy;
+    orc_table_geom(P, d, &dd, &R, &L->H, &side, &Cx, &Cy);
+    int64_t cap = orc_n_r(P, orc_nnz_c(P, side, Cx, Cy, R));
     L->level = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cap + 1));
     L->dx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cap + 1));
     L->dy = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cap + 1));
@@ -334,20 +374,47 @@ static orc_depth_list *orc_lut_get(orc_lut *t, int d) {
 }
 
 /* Build (force) the list of depth d in the cache; returns N_r,d. */
-int64_t orc_lut_build_depth(void *h, int d) { return orc_lut_get((orc_lut *)h, d)->n; }
+int64_t orc_lut_build_depth(void *h, int64_t d) { return orc_lut_get((orc_lut *)h, d)->n; }
 
-/* Reach of depth d's kept list (reading R-A19).  A level-l entry (dX, dY) of a point at (ix, iy)
+/* Table of a point (R-A20): t = iz in the standard mode, iz 4^L + (iy mod 2^L) 2^L + (ix mod 2^L)
+ * in the exact mode. */
+static int64_t orc_point_table(const orc_params *P, int64_t ix, int64_t iy, int iz) {
+    int b = orc_cls_bits(P);
+    int64_t m = ((int64_t)1 << b) - 1;
+    return ((int64_t)iz << (2 * b)) | ((iy & m) << b) | (ix & m);
+}
+
+/* Coefficient shift of a point (R-A8 standard, R-A20 exact): level-l target = s + (dX, dY). */
+static int64_t orc_shift(const orc_params *P, int64_t i, int l) {
+    if (P->exact) {
+        int64_t B = (int64_t)1 << P->levels;
+        return i - (i & (B - 1));
+    }
+    int64_t b = (int64_t)1 << l;
+    int64_t q = (i + (b >> 1)) / b;
+    if (((i + (b >> 1)) % b != 0) && (i + (b >> 1) < 0)) q--;
+    return b * q;
+}
+
+/* Reach of table d's kept list (reading R-A19; exact mode R-A20: no rounding term).  A level-l entry (dX, dY) of a point at (ix, iy)
  * lands at (s_l(ix) + dX, s_l(iy) + dY) (R-A8), and s_l(i) - i lies in (-2^(l-1), 2^(l-1)], so
  * with h = 2^(l-1) the target is within |dX| + h of ix and |dY| + h of iy.  Over the kept list:
  *   ek = max max(|dX|, |dY|) + h        (square bound)
  *   q  = max (|dX| + h)^2 + (|dY| + h)^2  (squared-distance bound)
  * The LL entries carry level L. */
-void orc_lut_reach(void *h, int d, int64_t *ek, int64_t *q) {
-    orc_depth_list *L = orc_lut_get((orc_lut *)h, d);
+void orc_lut_reach(void *h, int64_t d, int64_t *ek, int64_t *q) {
+    orc_lut *t = (orc_lut *)h;
+    orc_depth_list *L = orc_lut_get(t, d);
     int64_t e = 0, qq = 0;
+    int64_t cx = orc_table_cx(&t->P, d), cy = orc_table_cy(&t->P, d);
     for (int64_t k = 0; k < L->n; k++) {
-        int64_t hl = (int64_t)1 << (L->level[k] - 1);
-        int64_t ax = llabs((long long)L->dx[k]) + hl, ay = llabs((long long)L->dy[k]) + hl;
+        int64_t ax, ay;
+        if (t->P.exact) {   /* R-A20: the offset from the point is exactly (dX - cx, dY - cy) */
+            ax = llabs((long long)(L->dx[k] - cx)); ay = llabs((long long)(L->dy[k] - cy));
+        } else {
+            int64_t hl = (int64_t)1 << (L->level[k] - 1);
+            ax = llabs((long long)L->dx[k]) + hl; ay = llabs((long long)L->dy[k]) + hl;
+        }
         if (ax > e) e = ax;
         if (ay > e) e = ay;
         if (ax * ax + ay * ay > qq) qq = ax * ax + ay * ay;
@@ -405,8 +472,8 @@ static int orc_tile_in_footprint(int64_t ix, int64_t iy, int64_t ek, int64_t q, 
 }
 
 /* PAPER.md:115-122 sub-hologram re-basing, applied per T x T tile (R-A12): point j is in
- * bin(tx,ty) iff the tile is in its footprint (orc_tile_in_footprint with the reach ek[iz], q[iz]
- * of its depth) and lies in rows [row0, row1).  Brute force over all tiles of the band, points
+ * bin(tx,ty) iff the tile is in its footprint (orc_tile_in_footprint with the reach ek[t], q[t]
+ * of its table t = orc_point_table) and lies in rows [row0, row1).  Brute force over all tiles of the band, points
  * ascending.  tile_ptr has n_tiles+1 entries (tiles row-major within the band).  Returns total
  * entries, or -(needed) if cap is too small (idx untouched beyond cap). */
 int64_t orc_bins(const orc_params *P, int64_t T, const double *pts, int64_t n, int64_t row0, int64_t row1,
@@ -428,7 +495,7 @@ int64_t orc_bins(const orc_params *P, int64_t T, const double *pts, int64_t n, i
             tile_ptr[t] = total;
             for (int64_t j = 0; j < n; j++) {
                 if (!ok[j]) continue;
-                int64_t d = pp[3 * j + 2];
+                int64_t d = orc_point_table(P, pp[3 * j], pp[3 * j + 1], (int)pp[3 * j + 2]);
                 if (!orc_tile_in_footprint(pp[3 * j], pp[3 * j + 1], ek[d], q[d], X0, X1, Y0, Y1)) continue;
                 if (total < cap) idx[total] = (int32_t)j;
                 total++;
@@ -448,7 +515,8 @@ int64_t orc_bin_tile(const orc_params *P, int64_t T, const double *pts, int64_t 
         int64_t ix, iy;
         int iz;
         if (!orc_point(P, pts + 4 * j, &ix, &iy, &iz)) continue;
-        if (!orc_tile_in_footprint(ix, iy, ek[iz], q[iz], X0, X0 + T - 1, Y0, Y0 + T - 1)) continue;
+        int64_t d = orc_point_table(P, ix, iy, iz);
+        if (!orc_tile_in_footprint(ix, iy, ek[d], q[d], X0, X0 + T - 1, Y0, Y0 + T - 1)) continue;
         if (total < cap) idx[total] = (int32_t)j;
         total++;
     }
@@ -457,17 +525,12 @@ int64_t orc_bin_tile(const orc_params *P, int64_t T, const double *pts, int64_t 
 
 /* ---------------------------------------------------------------- WASABI (steps 2b, 3) */
 
-static int64_t orc_floor_div(int64_t a, int64_t b) {  /* b > 0 */
-    int64_t q = a / b;
-    if ((a % b != 0) && (a < 0)) q--;
-    return q;
-}
-
 /* Eq.(2), with the sub-hologram re-basing of PAPER.md:121-122 replaced by a
  * window [x0, x0+w) x [y0, y0+h) of the full hologram (R-A12: coefficients outside the window or
  * outside [0, N_h)^2 are dropped).  psi(m, n) = sum_j a_j sum_k c_{z_j,k} delta(...) with the
  * level shift s_l = 2^l floor((ix + 2^(l-1)) / 2^l) (R-A8).  psi: h x w interleaved complex,
- * overwritten.  Points ascending, list entries in canonical order (R-A11).
+ * overwritten.  Points ascending, list entries in canonical order (R-A11).  Exact mode (R-A20):
+ * the point's class table, every level shifted by s = (ix - cx, iy - cy).
  * Returns the number of in-window accumulations. */
 int64_t orc_wasabi_window(void *lut, const double *pts, int64_t n, int64_t x0, int64_t y0, int64_t w,
                           int64_t h, double *psi) {
@@ -482,13 +545,11 @@ int64_t orc_wasabi_window(void *lut, const double *pts, int64_t n, int64_t x0, i
         double R = orc_radius_px(P, orc_level_z(P, iz));
         int64_t E = (int64_t)ceil(R) + 3 * half;
         if (ix + E < x0 || ix - E >= x0 + w || iy + E < y0 || iy - E >= y0 + h) continue;
-        orc_depth_list *L = orc_lut_get(t, iz);
+        orc_depth_list *L = orc_lut_get(t, orc_point_table(P, ix, iy, iz));
         double a = pts[4 * j + 3];
         for (int64_t k = 0; k < L->n; k++) {
             int l = L->level[k];
-            int64_t b = (int64_t)1 << l, hb = b >> 1;
-            int64_t sx = b * orc_floor_div(ix + hb, b);
-            int64_t sy = b * orc_floor_div(iy + hb, b);
+            int64_t sx = orc_shift(P, ix, l), sy = orc_shift(P, iy, l);
             int64_t X = sx + L->dx[k], Y = sy + L->dy[k];
             if (X < 0 || X >= P->n_h || Y < 0 || Y >= P->n_h) continue;
             if (X < x0 || X >= x0 + w || Y < y0 || Y >= y0 + h) continue;

@@ -11,7 +11,7 @@ BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-                 "-I", CSRC, "-Xptxas", "-warn-spills"]
+                 "-I", CSRC, "-Xptxas", "-warn-spills"] + os.environ.get("WASABI_NVCC_DEFS", "").split()
 # the table kernels compute the fp32 rank keys with the specification's exact IEEE sequence
 PER_FILE = {"kernels_tables.cu": ["--fmad=false"], "kernels_direct.cu": ["--fmad=false"]}
 SOURCES = ["kernels_tables.cu", "kernels_scan.cu", "kernels_bins.cu", "kernels_superpose.cu",
@@ -21,7 +21,8 @@ SOURCES = ["kernels_tables.cu", "kernels_scan.cu", "kernels_bins.cu", "kernels_s
 def _stale(obj, src):
     if not os.path.exists(obj):
         return True
-    deps = [src, os.path.join(CSRC, "internal.h"), os.path.join(ROOT, "include", "wasabi.h")]
+    deps = [src, os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "device_common.cuh"),
+            os.path.join(ROOT, "include", "wasabi.h")]
     return any(os.path.getmtime(d) > os.path.getmtime(obj) for d in deps)
 
 

@@ -18,14 +18,37 @@ __host__ __device__ inline uint32_t pack_entry_pos(int X, int Y, int level) {
     return (uint32_t)X | ((uint32_t)Y << 14) | ((uint32_t)level << 28);
 }
 
-// Compact per-depth data read by the hot kernels (32 bytes).
+// Compact per-depth data read by the hot kernels (64 bytes).
 struct KDesc {
     int32_t H;                    // table half side
     int32_t E;                    // structural footprint bound ceil(R) + 3 2^(L-1) (buffer sizing)
     int32_t Ek;                   // kept reach, per axis (R-A19; computed by the table build)
     int32_t Q;                    // kept reach, squared distance (R-A19; computed by the table build)
-    int32_t ptr_base[kMaxLevels]; // level l (1..L) band pointer rows start at ptr_base[l-1]
+    int32_t ptr_base[kMaxLevels]; // canonical LUT: level l (1..L) band pointer rows start at ptr_base[l-1]
+    int32_t vptr_base[kMaxLevels];// window LUT: level l pointer rows start at vptr_base[l-1]
+    int32_t pad[2];
 };
+
+// ---- window LUT (the superposition kernel's copy of the kept lists) ----
+// A warp of the superposition kernel owns a 32-row strip of a T x T tile.  For a point and a
+// level l its strip is the table window rows [o, o + 32), o = strip_y0 - s_l(iy) + H, columns
+// [xs, xs + T), xs = tile_x0 - s_l(ix) + H.  o is a multiple of q_l = min(2^l, 32), so the
+// level-l entries are stored once per "variant" v = (o mod 32) / q_l in bands of exactly 32
+// rows [v q_l + 32 (k - 1), v q_l + 32 k): every strip window is exactly one band (no rows
+// outside the window are streamed).  Inside a band entries are ordered by column group of
+// G_l = max(8, 2^l) pixels with one int32 pointer per group boundary, so a window is one
+// contiguous entry range; for l <= 2 it may include up to kWinMargin columns on either side,
+// which land in the shared tile's margin columns (never read).
+constexpr int kWinRows = 32;
+#ifndef WASABI_WIN_MARGIN
+#define WASABI_WIN_MARGIN 6
+#endif
+constexpr int kWinMargin = WASABI_WIN_MARGIN;   // >= 6 (level-1 column-group overrun)
+__host__ __device__ inline int win_lq(int l) { return l < 5 ? l : 5; }          // log2 q_l
+__host__ __device__ inline int win_lg(int l) { return l < 3 ? 3 : l; }          // log2 G_l
+__host__ __device__ inline int win_variants(int l) { return kWinRows >> win_lq(l); }
+__host__ __device__ inline int win_bands(int side) { return (side + kWinRows - 1) / kWinRows + 1; }
+__host__ __device__ inline int win_cols(int side, int l) { return (side + (1 << win_lg(l)) - 1) >> win_lg(l); }
 
 // Per-depth data used by the table build and exports.
 struct DDesc {
@@ -37,7 +60,7 @@ struct DDesc {
     int32_t cta_base;   // prefix of K1 CTAs (tiles^2)
     int32_t group_base; // prefix of (level, band, Xb) groups (== its ptr_base for level 1)
     int32_t n_groups;
-    int32_t pad;
+    int32_t vgroup_base; // prefix of window-LUT pointer slots (== its vptr_base for level 1)
 };
 
 struct TableHeader {
@@ -50,8 +73,12 @@ struct TableHeader {
     int64_t kdesc_off, ddesc_off, ent_off, ptr_off, ctabase_off;  // byte offsets
     int64_t pad0;
     int64_t table_bytes;
+    int64_t total_vptrs;               // window-LUT int32 pointer slots
+    int64_t vent_cap;                  // window-LUT entry capacity (bound: 16 N_r per depth)
+    int64_t vptr_off, vval_off, vpos_off;  // window LUT: pointers, float2 values, uint16 positions
     int64_t pad[3];
 };
+static_assert(sizeof(TableHeader) <= 256, "table header must fit the 256-byte slot");
 
 struct BinHeader {
     uint64_t magic;
@@ -95,6 +122,7 @@ cudaError_t launch_select(const TableHeader &h, const void *d_tables, const uint
                           unsigned int *hist, unsigned long long *sel_state, int n_depth, cudaStream_t s);
 cudaError_t launch_groups(const TableHeader &h, void *d_tables, const float2 *coef_val, const uint32_t *coef_key,
                           const unsigned long long *sel_state, int pass, cudaStream_t s);
+cudaError_t launch_vgroups(const TableHeader &h, void *d_tables, int pass, cudaStream_t s);
 cudaError_t launch_scan_i32(int32_t *data, int64_t n, void *scratch, cudaStream_t s);
 cudaError_t launch_scan_u32_to_u64(const uint32_t *in, unsigned long long *out, int64_t n, void *scratch,
                                    cudaStream_t s);

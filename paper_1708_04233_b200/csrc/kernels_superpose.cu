@@ -3,23 +3,20 @@
 // with alpha = 2^-l for a level-l coefficient (reading R-A8: target X = s_l(ix) + dX,
 // s_l(i) = 2^l floor((i + 2^(l-1)) / 2^l)), in the interleaved in-place Haar layout (R-A6).
 //
-// Design (DESIGN.md §5 K4).  One CTA = one warp owns one T x T tile of psi in shared memory and
-// walks the tile's bin (points in ascending order).  For a point, the kept coefficients of level l
-// whose targets fall in the tile are found through the LUT's per-level band index: the tile window
-// is W x W blocks (W = T/2^l), covered by <= 5 bands, each one contiguous, X-exact entry range
-// ("slot"; <= 32 slots per point).  Per batch of kPB points:
-//   ranges   lane s computes slot s of each point (two independent points per step for ILP),
-//            compacts the non-empty ranges and scans their counts -> 8-byte range records
-//            (entry offset, smem base of the point's level) in shared memory;
-//   stream   the warp streams the flattened entries 32 at a time (a chunk never mixes points, so
-//            all targets of a chunk are distinct: no atomics, no races).  The current point's range
-//            prefixes live in registers (lane r holds range r); lane -> range uses one REDUX.OR
-//            marker + two POPCs; a kD-deep register ring prefetches the entry loads.
-// LUT entries are 16-byte records (pos = X | Y << 14 | level << 28, re, im, Y*S + X - pos):
-// target = pos + word3 + base (one IADD3; every word of the 128-bit load is used).
-// Rows outside the tile (band rounding) are rejected by one unsigned compare of the smem address
-// (X ranges are exact).  psi is written once, coalesced.  Per-pixel accumulation order is fixed
-// (point order): bitwise deterministic and independent of the band split.
+// Design (DESIGN.md §6 "Superpose").  One CTA owns one T x T tile of psi in shared memory and
+// walks the tile's bin (points in ascending order).  Warp w owns the pixels of level class
+// c = w & 1 ({1, 4, 5, 6} or {2, 3}; every Haar level occupies its own pixels) in the 32-row strip
+// w >> 1, so the warps of a CTA accumulate concurrently without atomics.  For a point and a level
+// of its class, the kept coefficients landing in the strip are ONE contiguous range of the window
+// LUT (internal.h: per-variant 32-row bands, column-group pointers), so a batch of 32 points
+// (lane = point) computes all its ranges with two pointer loads per (point, level), and the warp
+// then streams each range 32 entries per chunk: lane i of chunk c reads entry beg + 32 c + i
+// (float2 value + uint16 position) and does one read-modify-write in shared memory.  A chunk never
+// mixes points, so its targets are distinct; chunks run in point order for each level, so every
+// pixel (which belongs to exactly one level) accumulates in point order: bitwise deterministic
+// and independent of the band split (R-A11).  A kD-deep register ring keeps the entry loads of
+// the next chunks in flight across range, level and batch boundaries.  Column overrun of the
+// level-1/2 column groups lands in kWinMargin margin columns of the shared tile (never read).
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -30,14 +27,27 @@ namespace wasabi {
 namespace {
 
 struct SupArgs {
-    int T, S, L, tiles_x;
+    int L, tiles_x;
     int64_t row0, n_h;
 };
 
-constexpr int kPB = 8;                 // points per range batch
-constexpr int kD = 4;                  // prefetch depth (chunks)
-constexpr int kEmpty = 0x3fffffff;
-constexpr int kBadBase = 0x3fffffff;   // base of padding lanes: address always >= T*S
+#ifndef WASABI_KD
+#define WASABI_KD 4
+#endif
+#ifndef WASABI_MINB
+#define WASABI_MINB 6
+#endif
+#ifndef WASABI_PF
+#define WASABI_PF 1
+#endif
+constexpr int kD = WASABI_KD;          // register ring depth (chunks in flight per warp)
+
+// Bulk prefetch of [p, p + bytes) into L2 (16-byte granules): one instruction per range, so the
+// later chunks of a range hit L2 instead of waiting on DRAM.
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ float2 lds2(uint32_t a) {
     float2 v;
@@ -48,24 +58,21 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
 
-// level class c: c = 0 -> {1} U {4..L}, c = 1 -> {2, 3} (pixel-disjoint in the interleaved layout)
-__device__ __forceinline__ bool in_class(int c, int l) { return c == 0 ? (l == 1 || l >= 4) : (l == 2 || l == 3); }
+// levels of class c, slot j (0 = none): c = 0 -> {1, 4, 5, 6}, c = 1 -> {2, 3}
+__device__ __forceinline__ int class_level(int c, int j, int L) {
+    const int l = c == 0 ? (j == 0 ? 1 : j + 3) : (j < 2 ? j + 2 : 0);
+    return l <= L ? l : 0;
+}
 
-// Warp w owns (level class c = w & 1) x (tile row half h = w >> 1): pixel-disjoint, so the four
-// warps of a CTA accumulate into the shared tile concurrently.  SEGW lanes per point: each range
-// step handles 32/SEGW points.
-template <int SEGW>
-__global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restrict__ d_bins,
-                                                           const void *__restrict__ d_tables, SupArgs A,
-                                                           float2 *__restrict__ psi, int fused, QArgs qa,
-                                                           uint8_t *__restrict__ bits) {
-    constexpr int PPS = 32 / SEGW;            // points per range step
-    constexpr int kH = kPB / PPS;             // range steps per batch
-    extern __shared__ float2 tile[];          // T x S (+4 scratch)
-    __shared__ int2 rec_all[4][kPB][SEGW];    // (entry offset = beg - excl, base | shift << 23)
-    __shared__ int ex_all[4][kPB][SEGW];      // exclusive prefix (kEmpty past the last range)
-    __shared__ int tot_all[4][kPB];
-    __shared__ float a_all[4][kPB];
+template <int T>
+__global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_kernel(const void *__restrict__ d_bins,
+                                                                           const void *__restrict__ d_tables,
+                                                                           SupArgs A, float2 *__restrict__ psi,
+                                                                           int fused, QArgs qa,
+                                                                           uint8_t *__restrict__ bits) {
+    constexpr int M = kWinMargin, S = T + M, NT = 2 * T;
+    constexpr int kData = M + T * S + M;      // margin-padded tile; per-warp dummy cells follow
+    extern __shared__ float2 tile[];
     const char *bb = reinterpret_cast<const char *>(d_bins);
     const BinHeader *bh = reinterpret_cast<const BinHeader *>(bb);
     const int4 *__restrict__ pconv = reinterpret_cast<const int4 *>(bb + bh->pts_off);
@@ -74,210 +81,181 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
     const char *tb = reinterpret_cast<const char *>(d_tables);
     const TableHeader *th = reinterpret_cast<const TableHeader *>(tb);
     const KDesc *__restrict__ kd = reinterpret_cast<const KDesc *>(tb + th->kdesc_off);
-    const int32_t *__restrict__ tptr = reinterpret_cast<const int32_t *>(tb + th->ptr_off);
-    const uint4 *__restrict__ tent = reinterpret_cast<const uint4 *>(tb + th->ent_off);
+    const int32_t *__restrict__ vptr = reinterpret_cast<const int32_t *>(tb + th->vptr_off);
+    const float2 *__restrict__ vval = reinterpret_cast<const float2 *>(tb + th->vval_off);
+    const uint16_t *__restrict__ vpos = reinterpret_cast<const uint16_t *>(tb + th->vpos_off);
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int cls = wid & 1, half = wid >> 1;
-    const int T = A.T, S = A.S, TS = T * S, Th = T / 2;
+    const int cls = wid & 1, strip = wid >> 1;
     const int64_t t = blockIdx.x;
     const int tile_x0 = (int)(t % A.tiles_x) * T;
     const int tile_y0 = (int)(A.row0 + (t / A.tiles_x) * (int64_t)T);
-    const int sub_y0 = tile_y0 + half * Th;          // this warp's rows [sub_y0, sub_y0 + Th)
-    const int sub_lo = half * Th * S;                // its smem address range [sub_lo, sub_lo + Th*S)
-    const unsigned lanemask_lt = (1u << lane) - 1u;
-    const unsigned lanemask_le = lanemask_lt | (1u << lane);
+    const int strip_y0 = tile_y0 + kWinRows * strip;
+    const int strip_base = M + kWinRows * strip * S;   // smem index of (strip row 0, column 0)
+    const int dummy = kData + wid;
     const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(tile);
-    const uint32_t dummy_sa = tile_sa + 8u * (uint32_t)(TS + wid);
-    int2(*rec_s)[SEGW] = rec_all[wid];
-    int(*ex_s)[SEGW] = ex_all[wid];
-    int *tot_s = tot_all[wid];
-    float *a_s = a_all[wid];
 
-    for (int i = threadIdx.x; i < TS; i += 128) tile[i] = make_float2(0.f, 0.f);
-
-    // lane = (segment seg: which point of a step, slot) -> (level, band slot k) of this class
-    const int seg = lane / SEGW, slot = lane % SEGW;
-    int my_l = 0, my_k = 0;
-    {
-        int base = 0;
-        for (int l = 1; l <= A.L; l++) {
-            if (!in_class(cls, l)) continue;
-            const int hb = band_blocks(T, l);
-            const int yb_lo = sub_y0 >> l, yb_hi = ((sub_y0 + Th - 1) >> l) + 1;
-            const int Wy = yb_hi - yb_lo;
-            const int m = (hb == 1) ? Wy : (Wy + hb - 1) / hb + 1;
-            if (slot >= base && slot < base + m) { my_l = l; my_k = slot - base; }
-            base += m;
-        }
-    }
-    const bool has_slot = my_l > 0;
-    const int l_ = has_slot ? my_l : 1;
-    const int my_half = 1 << (l_ - 1);
-    const int my_hb = band_blocks(T, l_);
-    const int my_lhb = 31 - __clz(my_hb);
-    const int my_Wx = T >> l_;
-    const int my_tx = tile_x0 >> l_;
-    const int my_ty = sub_y0 >> l_;
-    const int my_Wy = (((sub_y0 + Th - 1) >> l_) + 1) - my_ty;
-    const unsigned seg_bits = SEGW == 32 ? 0xffffffffu : ((1u << SEGW) - 1u);
-    const unsigned seg_lt = ((1u << slot) - 1u) << (seg * SEGW);
+    for (int i = threadIdx.x; i < kData + NT / 32; i += NT) tile[i] = make_float2(0.f, 0.f);
     __syncthreads();
 
-    const unsigned long long b0 = bptr[t], b1 = bptr[t + 1];
-    unsigned long long pb = b0;      // next point of the bin to load
-    int np = 0;                      // non-empty points in the current batch
-    int4 q = make_int4(0, 0, 0, 0);
+    const int lv0 = class_level(cls, 0, A.L), lv1 = class_level(cls, 1, A.L);
+    const int lv2 = class_level(cls, 2, A.L), lv3 = class_level(cls, 3, A.L);
+    const unsigned long long b1 = bptr[t + 1];
+    unsigned long long pb = bptr[t];
 
-    auto load_batch = [&]() {
-        np = 0;
-        while (np == 0 && pb < b1) {
-            const int nq = (int)min((unsigned long long)kPB, b1 - pb);
-            q = make_int4(0, 0, 0, 0);
-            if (lane < nq) q = __ldg(pconv + __ldg(bidx + pb + lane));
-            pb += nq;
-            int ix[kH], iy[kH], H[kH], pbs[kH];
-#pragma unroll
-            for (int h = 0; h < kH; h++) {
-                const int k = PPS * h + seg;
-                ix[h] = __shfl_sync(0xffffffffu, q.x, k);
-                iy[h] = __shfl_sync(0xffffffffu, q.y, k);
-                const int iz = __shfl_sync(0xffffffffu, q.z, k);
-                H[h] = 0; pbs[h] = 0;
-                if (k < nq && has_slot) { H[h] = __ldg(&kd[iz].H); pbs[h] = __ldg(&kd[iz].ptr_base[l_ - 1]); }
-            }
-            int beg[kH], end[kH], bse[kH];
-#pragma unroll
-            for (int h = 0; h < kH; h++) {
-                const int k = PPS * h + seg;
-                const int sx = (ix[h] + my_half) >> l_, sy = (iy[h] + my_half) >> l_;   // floor
-                const int Hb = H[h] >> l_, nb = (2 * H[h]) >> l_;
-                const int xb0 = my_tx - sx + Hb, yb0 = my_ty - sy + Hb;
-                const int xb0c = max(xb0, 0), xb1c = min(xb0 + my_Wx, nb);
-                const int yb0c = max(yb0, 0), yb1c = min(yb0 + my_Wy, nb);
-                const int band = (yb0c >> my_lhb) + my_k;
-                const bool ok = k < nq && has_slot && xb0c < xb1c && yb0c < yb1c && band * my_hb < yb1c;
-                const int row = pbs[h] + band * (nb + 1);
-                beg[h] = 0; end[h] = 0;
-                if (ok) { beg[h] = __ldg(tptr + row + xb0c); end[h] = __ldg(tptr + row + xb1c); }
-                bse[h] = ((sy << l_) - H[h] - tile_y0) * S + ((sx << l_) - H[h] - tile_x0);
-            }
-#pragma unroll
-            for (int h = 0; h < kH; h++) {
-                const int c = end[h] - beg[h];
-                const unsigned bal = __ballot_sync(0xffffffffu, c > 0);
-                if (bal == 0u) continue;
-                int incl = c;
-#pragma unroll
-                for (int o = 1; o < SEGW; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, incl, o, SEGW);
-                    if (slot >= o) incl += y;
-                }
-                const int excl = incl - c;
-                // compacted index of my segment's point among the non-empty points of this step
-                const unsigned nonempty_segs = [&] {
-                    unsigned m = 0;
-#pragma unroll
-                    for (int g = 0; g < PPS; g++) m |= ((bal >> (g * SEGW)) & seg_bits) ? (1u << g) : 0u;
-                    return m;
-                }();
-                const unsigned mine = (bal >> (seg * SEGW)) & seg_bits;
-                const int idx = np + __popc(nonempty_segs & ((1u << seg) - 1u));
-                if (mine) {
-                    if (c > 0) {
-                        const int p = __popc(bal & seg_lt);
-                        rec_s[idx][p] = make_int2(beg[h] - excl, bse[h]);
-                        ex_s[idx][p] = excl;
-                    }
-                    if (slot >= __popc(mine)) ex_s[idx][slot] = kEmpty;
-                    if (slot == SEGW - 1) tot_s[idx] = incl;
-                }
-                const float aw = __int_as_float(__shfl_sync(0xffffffffu, q.w, PPS * h + seg));
-                if (mine && slot == 0) a_s[idx] = aw;
-                np += __popc(nonempty_segs);
-            }
+    // batch state: lane = point; per level slot j its range (beg, len) and smem base
+    float a_l = 0.f;
+    int beg[4], len[4], base[4];
+    unsigned msk[4];
+    auto range = [&](int l, int ix, int iy, int H, int d, bool ok, int &b, int &n, int &bs) {
+        b = 0; n = 0; bs = 0;
+        if (l == 0) return;
+        const int h = 1 << (l - 1), side = 2 * H;
+        const int sx = ((ix + h) >> l) << l, sy = ((iy + h) >> l) << l;
+        const int o = strip_y0 - sy + H;                 // window rows [o, o + 32)
+        const int xs = tile_x0 - sx + H;                 // window columns [xs, xs + T)
+        ok = ok && o > -kWinRows && o < side && xs > -T && xs < side;
+        const int lq = win_lq(l), lg = win_lg(l);
+        const int v = (o & (kWinRows - 1)) >> lq;
+        const int k = (o - (v << lq) + kWinRows) >> 5;
+        const int ncol = win_cols(side, l);
+        const int xa = max(xs >> lg, 0), xb = min((xs + T + (1 << lg) - 1) >> lg, ncol);
+        if (ok && xa < xb) {
+            const int row = __ldg(&kd[d].vptr_base[l - 1]) + (v * win_bands(side) + k) * (ncol + 1);
+            b = __ldg(vptr + row + xa);
+            n = __ldg(vptr + row + xb) - b;
         }
-        __syncwarp();
+        bs = strip_base - xs;
+    };
+    auto load_batch = [&]() -> bool {
+        while (pb < b1) {
+            const int nq = (int)min((unsigned long long)32, b1 - pb);
+            const bool ok = lane < nq;
+            int4 q = make_int4(0, 0, 0, 0);
+            int H = 0;
+            if (ok) {
+                q = __ldg(pconv + __ldg(bidx + pb + lane));
+                H = __ldg(&kd[q.z].H);
+            }
+            pb += nq;
+            a_l = __int_as_float(q.w);
+            range(lv0, q.x, q.y, H, q.z, ok, beg[0], len[0], base[0]);
+            range(lv1, q.x, q.y, H, q.z, ok, beg[1], len[1], base[1]);
+            range(lv2, q.x, q.y, H, q.z, ok, beg[2], len[2], base[2]);
+            range(lv3, q.x, q.y, H, q.z, ok, beg[3], len[3], base[3]);
+            bool any = false;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                msk[j] = __ballot_sync(kFull, len[j] > 0);
+                any |= msk[j] != 0u;
+                if (WASABI_PF && len[j] > 0) {
+                    const int e0 = beg[j] & ~1, e1 = (beg[j] + len[j] + 1) & ~1;   // 16-byte granules
+                    prefetch_l2(vval + e0, 8u * (uint32_t)(e1 - e0));
+                    const int p0 = beg[j] & ~7, p1 = (beg[j] + len[j] + 7) & ~7;
+                    prefetch_l2(vpos + p0, 2u * (uint32_t)(p1 - p0));
+                }
+            }
+            if (any) return true;
+        }
+        return false;
     };
 
-    // prefetch cursor (warp-uniform except exv)
-    int kp = 0, cp = 0, totp = 0, exv = kEmpty;
-    float ap = 0.f;
-    load_batch();
-    if (np > 0) { totp = tot_s[0]; exv = lane < SEGW ? ex_s[0][lane] : kEmpty; ap = a_s[0]; }
-    bool done = np == 0;
+    // chunk generator (warp-uniform): level slot gj, remaining points gm, current range
+    int gj = 0, c_beg = 0, c_end = 0;
+    uint32_t c_sa = 0u;
+    unsigned gm = 0u;
+    float c_a = 0.f;
+    bool have = false;
+    int s_beg = 0, s_len = 0, s_base = 0;   // this lane's range for slot gj
+    auto select_slot = [&]() {
+        gm = gj == 0 ? msk[0] : gj == 1 ? msk[1] : gj == 2 ? msk[2] : msk[3];
+        s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : gj == 2 ? beg[2] : beg[3];
+        s_len = gj == 0 ? len[0] : gj == 1 ? len[1] : gj == 2 ? len[2] : len[3];
+        s_base = gj == 0 ? base[0] : gj == 1 ? base[1] : gj == 2 ? base[2] : base[3];
+    };
+    auto next_range = [&]() {
+        while (gm == 0u) {
+            if (++gj >= 4) {
+                if (!load_batch()) { have = false; return; }
+                gj = 0;
+            }
+            select_slot();
+        }
+        const int p = __ffs(gm) - 1;
+        gm &= gm - 1u;
+        c_beg = __shfl_sync(kFull, s_beg, p);
+        c_end = c_beg + __shfl_sync(kFull, s_len, p);
+        c_sa = tile_sa + 8u * (uint32_t)__shfl_sync(kFull, s_base, p);
+        c_a = __shfl_sync(kFull, a_l, p);
+        have = true;
+    };
+    if (load_batch()) {
+        gj = 0;
+        select_slot();
+        next_range();
+    }
 
-    uint32_t rw[kD], rz[kD];
-    float rx[kD], ry[kD], ra[kD];
-    int rb[kD];
+    // ring slot: value, position, smem byte base of the range (dummy cell for idle lanes), a_j;
+    // an idle lane's value is stale but finite-or-not, it only ever reaches its dummy cell
+    const uint32_t dummy_sa = tile_sa + 8u * (uint32_t)dummy;
+    float2 rv[kD];
+    int rp[kD];
+    uint32_t rb[kD];
+    float ra[kD];
 #pragma unroll
-    for (int s = 0; s < kD; s++) { rw[s] = 0; rz[s] = 0; rx[s] = 0.f; ry[s] = 0.f; ra[s] = 0.f; }
-#define WASABI_PREFETCH(s)                                                                  \
-    do {                                                                                    \
-        rb[s] = kBadBase;                                                                   \
-        if (kp < np) {                                                                      \
-            unsigned m = ((unsigned)(exv - cp - 1) < 31u) ? (1u << (exv - cp)) : 0u;        \
-            m = __reduce_or_sync(0xffffffffu, m);                                           \
-            const int rr = __popc(__ballot_sync(0xffffffffu, exv <= cp)) - 1 +              \
-                           __popc(m & lanemask_le);                                         \
-            const int e = cp + lane;                                                        \
-            const int2 d = rec_s[kp][rr & (SEGW - 1)];                                      \
-            if (e < totp) {                                                                 \
-                const uint4 en = __ldg(tent + e + d.x);                                     \
-                rw[s] = en.x; rx[s] = __uint_as_float(en.y); ry[s] = __uint_as_float(en.z); rz[s] = en.w; \
-                rb[s] = d.y; ra[s] = ap;                                                    \
-            }                                                                               \
-            cp += 32;                                                                       \
-            if (cp >= totp) {                                                               \
-                cp = 0;                                                                     \
-                if (++kp < np) {                                                            \
-                    totp = tot_s[kp]; exv = lane < SEGW ? ex_s[kp][lane] : kEmpty; ap = a_s[kp]; \
-                }                                                                           \
-            }                                                                               \
-        }                                                                                   \
+    for (int s = 0; s < kD; s++) rv[s] = make_float2(0.f, 0.f);
+#define WASABI_PREFETCH(s)                                                          \
+    do {                                                                            \
+        const int e = c_beg + lane;                                                 \
+        const bool v = have && e < c_end;                                           \
+        rp[s] = 0;                                                                  \
+        if (v) {                                                                    \
+            rv[s] = __ldg(vval + e);                                                \
+            rp[s] = __ldg(vpos + e);                                                \
+        }                                                                           \
+        rb[s] = v ? c_sa : dummy_sa;                                                \
+        ra[s] = c_a;                                                                \
+        if (have) {                                                                 \
+            c_beg += 32;                                                            \
+            if (c_beg >= c_end) next_range();                                       \
+        }                                                                           \
     } while (0)
-#define WASABI_CONSUME(s)                                                                   \
-    do {                                                                                    \
-        const int addr = (int)(rw[s] + rz[s]) + rb[s];                                       \
-        const uint32_t sa = (unsigned)(addr - sub_lo) < (unsigned)(Th * S)                  \
-                                ? tile_sa + 8u * (uint32_t)addr : dummy_sa;                 \
-        float2 o = lds2(sa);                                                                \
-        o.x = fmaf(ra[s], rx[s], o.x);                                                      \
-        o.y = fmaf(ra[s], ry[s], o.y);                                                      \
-        sts2(sa, o);                                                                        \
+#define WASABI_CONSUME(s)                                                           \
+    do {                                                                            \
+        const uint32_t sa = rb[s] + 8u * (uint32_t)rp[s];                           \
+        float2 o = lds2(sa);                                                        \
+        o.x = fmaf(ra[s], rv[s].x, o.x);                                            \
+        o.y = fmaf(ra[s], rv[s].y, o.y);                                            \
+        sts2(sa, o);                                                                \
     } while (0)
 #pragma unroll
     for (int s = 0; s < kD; s++) WASABI_PREFETCH(s);
-    while (true) {
+    bool more = true;
+    while (more) {
+        more = have;
 #pragma unroll
         for (int s = 0; s < kD; s++) {
             WASABI_CONSUME(s);
             WASABI_PREFETCH(s);
         }
-        if (done) break;
-        if (kp >= np) {
-            load_batch();
-            kp = 0; cp = 0;
-            if (np > 0) { totp = tot_s[0]; exv = lane < SEGW ? ex_s[0][lane] : kEmpty; ap = a_s[0]; }
-            else done = true;     // one more round drains the ring
-        }
     }
 #undef WASABI_PREFETCH
 #undef WASABI_CONSUME
     __syncthreads();
+    float2 *data = tile + M;                    // row r, column x at data[r * S + x]
     if (fused) {
         // steps 3 (+4) in place: psi never leaves shared memory
-        inverse_haar_tile(tile, T, S, A.L, threadIdx.x, 128);
+        inverse_haar_tile(data, T, S, A.L, threadIdx.x, NT);
         if (bits) {
-            const int bpr = T / 8;
-            for (int bi = threadIdx.x; bi < T * bpr; bi += 128) {
+            constexpr int bpr = T / 8;
+            for (int bi = threadIdx.x; bi < T * bpr; bi += NT) {
                 const int row = bi / bpr, xb = bi % bpr;
                 const int64_t Y = tile_y0 + row;
                 unsigned byte = 0;
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
                     const int x = xb * 8 + i;
-                    const float I = interference(tile[row * S + x], tile_x0 + x, Y, qa);
+                    const float I = interference(data[row * S + x], tile_x0 + x, Y, qa);
                     byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
                 }
                 bits[(Y - A.row0) * (A.n_h / 8) + tile_x0 / 8 + xb] = (uint8_t)byte;
@@ -286,8 +264,22 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
         if (!psi) return;
     }
     float2 *out = psi + (int64_t)(tile_y0 - A.row0) * A.n_h + tile_x0;
-    for (int y = wid; y < T; y += 4)
-        for (int x = lane; x < T; x += 32) out[(int64_t)y * A.n_h + x] = tile[y * S + x];
+    for (int y = wid; y < T; y += NT / 32)
+        for (int x = lane; x < T; x += 32) out[(int64_t)y * A.n_h + x] = data[y * S + x];
+}
+
+template <int T>
+cudaError_t launch_t(const void *d_bins, const void *d_tables, const SupArgs &A, int64_t n_tiles, float2 *psi,
+                     int fused, const QArgs &qa, uint8_t *bits, cudaStream_t s) {
+    constexpr int M = kWinMargin, S = T + M;
+    const int smem = (M + T * S + M + T / 16) * (int)sizeof(float2);
+    cudaError_t e = cudaFuncSetAttribute(superpose_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (n_tiles > 0) {
+        count_launches(1);
+        superpose_kernel<T><<<(unsigned)n_tiles, 2 * T, smem, s>>>(d_bins, d_tables, A, psi, fused, qa, bits);
+    }
+    return cudaGetLastError();
 }
 
 }  // namespace
@@ -295,20 +287,13 @@ __global__ void __launch_bounds__(128, 6) superpose_kernel(const void *__restric
 cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x, int tiles_y,
                              int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
                              uint8_t *bits, cudaStream_t s) {
-    const int smem = (T * S + 4) * (int)sizeof(float2);
-    // range slots per (class, row half) and point: <= 8 for T = 64, <= 16 for T = 128
-    auto kern = T <= 64 ? superpose_kernel<8> : superpose_kernel<16>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
+    if (S != T + kWinMargin) return cudaErrorInvalidValue;
     SupArgs A;
-    A.T = T; A.S = S; A.L = L; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
+    A.L = L; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
     const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
-    if (n_tiles > 0) {
-        count_launches(1);
-        kern<<<(unsigned)n_tiles, 128, smem, s>>>(d_bins, d_tables, A, psi, fused,
-                                                  make_qargs(print4, pitch, n_h), bits);
-    }
-    return cudaGetLastError();
+    const QArgs qa = make_qargs(print4, pitch, n_h);
+    return T <= 64 ? launch_t<64>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s)
+                   : launch_t<128>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s);
 }
 
 }  // namespace wasabi

@@ -219,13 +219,7 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
                     if (key >= thr) {
                         if (pass) {
                             const float2 v = coef_val[o];
-                            // word 3 = (Y*S + X) - pos (mod 2^32): the superpose kernel forms the
-                            // shared-memory offset as pos + word3 + base in one add, and no word of
-                            // the 128-bit load is dead (a dead word is a write-after-write hazard
-                            // on the in-flight load once its register is reused)
-                            const uint32_t pos = pack_entry_pos(X, Y, l);
-                            const uint32_t off = (uint32_t)(Y * (T + 1) + X);
-                            ent[out] = make_uint4(pos, __float_as_uint(v.x), __float_as_uint(v.y), off - pos);
+                            ent[out] = make_uint4(pack_entry_pos(X, Y, l), __float_as_uint(v.x), __float_as_uint(v.y), 0u);
                             out++;
                         } else {
                             // target within |dX| + 2^(l-1) of the point per axis (s_l(i) - i in (-h, h])
@@ -255,7 +249,76 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
     }
 }
 
+// K2d: the superposition kernel's window LUT (internal.h), re-grouped from the canonical lists.
+// One thread per pointer slot (depth, level, variant v, band k, column group xg): it visits the
+// canonical (band, Xb) ranges that cover rows [bs, bs + 32), bs = v q_l + 32 (k - 1), and columns
+// [xg G_l, (xg + 1) G_l), and counts (pass 0) or writes (pass 1) the entries whose row falls in
+// the band: value (float2) and position (Y - bs) S + X (uint16), in canonical order.
+__global__ void __launch_bounds__(256) vgroups_kernel(void *tables, int n_depth, int L, int T, int S, int pass) {
+    const TableHeader &h = hdr(tables);
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= h.total_vptrs) return;
+    const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
+    const KDesc *kd = at<KDesc>(tables, h.kdesc_off);
+    int32_t *vptr = atw<int32_t>(tables, h.vptr_off);
+    int lo = 0, hi = n_depth;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (dd[mid].vgroup_base <= g) lo = mid; else hi = mid;
+    }
+    const int d = lo;
+    const KDesc K = kd[d];
+    const int side = dd[d].side;
+    int l = 1;
+    while (l < L && K.vptr_base[l] <= g) l++;
+    const int ncol = win_cols(side, l), nband = win_bands(side);
+    const int64_t local = g - K.vptr_base[l - 1];
+    const int xg = (int)(local % (ncol + 1));
+    if (xg == ncol) {  // dummy slot: band end
+        if (pass == 0) vptr[g] = 0;
+        return;
+    }
+    const int row = (int)(local / (ncol + 1));
+    const int v = row / nband, k = row % nband;
+    const int bs = (v << win_lq(l)) + kWinRows * (k - 1);
+    const int y0 = max(bs, 0), y1 = min(bs + kWinRows, side);
+    const int lg = win_lg(l);
+    const int nb = side >> l, bh = band_blocks(T, l) << l;              // canonical band height (px)
+    const int xb0 = (xg << lg) >> l, xb1 = min(((xg + 1) << lg) >> l, nb);  // canonical block columns
+    const int32_t *ptr = at<int32_t>(tables, h.ptr_off);
+    const uint4 *ent = at<uint4>(tables, h.ent_off);
+    float2 *vval = atw<float2>(tables, h.vval_off);
+    uint16_t *vpos = atw<uint16_t>(tables, h.vpos_off);
+    int out = pass ? vptr[g] : 0, cnt = 0;
+    if (y0 < y1) {
+        for (int cb = y0 / bh; cb <= (y1 - 1) / bh; cb++) {
+            const int crow = K.ptr_base[l - 1] + cb * (nb + 1);
+            const int e0 = ptr[crow + xb0], e1 = ptr[crow + xb1];
+            for (int e = e0; e < e1; e++) {
+                const uint4 en = ent[e];
+                const int Y = (int)((en.x >> 14) & 0x3fffu), X = (int)(en.x & 0x3fffu);
+                if (Y < bs || Y >= bs + kWinRows) continue;
+                if (pass) {
+                    vval[out] = make_float2(__uint_as_float(en.y), __uint_as_float(en.z));
+                    vpos[out] = (uint16_t)((Y - bs) * S + X);
+                    out++;
+                }
+                cnt++;
+            }
+        }
+    }
+    if (pass == 0) vptr[g] = cnt;
+}
+
 }  // namespace
+
+cudaError_t launch_vgroups(const TableHeader &h, void *d_tables, int pass, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((h.total_vptrs + 255) / 256);
+    if (blocks == 0) return cudaSuccess;
+    count_launches(1);
+    vgroups_kernel<<<blocks, 256, 0, s>>>(d_tables, h.n_depth, h.levels, h.tile, h.S, pass);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_psf_haar(const TableHeader &h, const void *d_tables, float2 *coef_val, uint32_t *coef_key,
                             double k, double pitch, int levels, int n_depth, cudaStream_t s) {

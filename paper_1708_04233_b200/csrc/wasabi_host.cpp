@@ -133,7 +133,7 @@ struct Geo {
     std::vector<KDesc> kd;
     std::vector<DDesc> dd;
     std::vector<int32_t> ctabase;
-    int64_t total_entries = 0, total_ptrs = 0, total_ctas = 0, total_coef = 0, max_E = 0;
+    int64_t total_entries = 0, total_ptrs = 0, total_ctas = 0, total_coef = 0, max_E = 0, total_vptrs = 0;
     TableHeader th;
     size_t table_bytes = 0, scratch_bytes = 0;
     size_t sc_val = 0, sc_key = 0, sc_hist = 0, sc_sel = 0, sc_scan = 0;
@@ -148,7 +148,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     wasabi_status st = validate(P);
     if (st != WASABI_OK) return st;
     g.P = *P;
-    g.T = P->tile; g.S = P->tile + 1; g.L = P->levels; g.nd = P->n_depth;
+    g.T = P->tile; g.S = P->tile + kWinMargin; g.L = P->levels; g.nd = P->n_depth;
     g.k = 2.0 * kPi / P->wavelength_m;
     const double sigma = P->wavelength_m / (2.0 * P->pitch_m);
     g.tan_theta = sigma / std::sqrt(1.0 - sigma * sigma);
@@ -157,7 +157,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     g.dd.assign(g.nd, DDesc{});
     g.ctabase.assign(g.nd + 1, 0);
     const int64_t B = 1ll << g.L;
-    int64_t ptr = 0, ctas = 0, coef = 0, entries = 0;
+    int64_t ptr = 0, ctas = 0, coef = 0, entries = 0, vptr = 0;
     for (int d = 0; d < g.nd; d++) {
         const double z = level_z(*P, g.dz, d);
         const double R = std::fabs(z) * g.tan_theta / P->pitch_m;
@@ -187,6 +187,13 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
         }
         for (int l = g.L + 1; l <= kMaxLevels; l++) K.ptr_base[l - 1] = (int32_t)ptr;
         D.n_groups = (int32_t)(ptr - D.group_base);
+        // window LUT pointer rows: per level, variants x bands x (column groups + 1)
+        D.vgroup_base = (int32_t)vptr;
+        for (int l = 1; l <= g.L; l++) {
+            K.vptr_base[l - 1] = (int32_t)vptr;
+            vptr += (int64_t)win_variants(l) * win_bands(D.side) * (win_cols(D.side, l) + 1);
+        }
+        for (int l = g.L + 1; l <= kMaxLevels; l++) K.vptr_base[l - 1] = (int32_t)vptr;
         D.nnz = nnz_structural(H, R, g.L);
         {
             const int64_t r_ppm = llround(P->retention * 1e6);
@@ -194,11 +201,12 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
             D.n_r = std::min(n, D.nnz);
         }
         entries += D.n_r;
-        if (ptr > (int64_t)INT32_MAX / 2 || entries > (int64_t)INT32_MAX / 2 || ctas > (int64_t)INT32_MAX / 2)
+        if (ptr > (int64_t)INT32_MAX / 2 || entries > (int64_t)INT32_MAX / 32 || ctas > (int64_t)INT32_MAX / 2 ||
+            vptr > (int64_t)INT32_MAX / 2)
             return fail(WASABI_EINVAL, "table too large for 32-bit indices");
     }
     g.ctabase[g.nd] = (int32_t)ctas;
-    g.total_entries = entries; g.total_ptrs = ptr; g.total_ctas = ctas; g.total_coef = coef;
+    g.total_entries = entries; g.total_ptrs = ptr; g.total_ctas = ctas; g.total_coef = coef; g.total_vptrs = vptr;
     // table buffer layout
     TableHeader &h = g.th;
     std::memset(&h, 0, sizeof h);
@@ -212,6 +220,12 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     h.ctabase_off = off; off = align_up(off + 4 * (g.nd + 1), 256);
     h.ptr_off = off; off = align_up(off + 4 * (size_t)(ptr + 1), 256);
     h.ent_off = off; off = align_up(off + 16 * (size_t)entries, 256);
+    // window LUT: a level-l entry is stored once per variant (<= 16 copies)
+    h.total_vptrs = vptr;
+    h.vent_cap = 16 * entries;
+    h.vptr_off = off; off = align_up(off + 4 * (size_t)(vptr + 1), 256);
+    h.vval_off = off; off = align_up(off + 8 * (size_t)h.vent_cap, 256);
+    h.vpos_off = off; off = align_up(off + 2 * (size_t)h.vent_cap, 256);
     h.table_bytes = off;
     g.table_bytes = off;
     // build scratch
@@ -220,7 +234,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     g.sc_key = so; so = align_up(so + 4 * (size_t)coef, 256);
     g.sc_hist = so; so = align_up(so + 4 * 256 * (size_t)g.nd, 256);
     g.sc_sel = so; so = align_up(so + 24 * (size_t)g.nd, 256);
-    g.sc_scan = so; so = align_up(so + scan_scratch_bytes(ptr + 1), 256);
+    g.sc_scan = so; so = align_up(so + scan_scratch_bytes(std::max(ptr, vptr) + 1), 256);
     g.scratch_bytes = so;
     return WASABI_OK;
 }
@@ -320,6 +334,12 @@ wasabi_status wasabi_build_psf_tables(const wasabi_params *params, void *d_table
     CK(launch_scan_i32(reinterpret_cast<int32_t *>(tb + g.th.ptr_off), g.total_ptrs + 1, sb + g.sc_scan, stream),
        "scan ptr");
     CK(launch_groups(g.th, d_tables, cval, ckey, sel, 1, stream), "groups scatter");
+    // the superposition kernel's window LUT, re-grouped from the canonical lists
+    CK(cudaMemsetAsync(tb + g.th.vptr_off, 0, 4 * (size_t)(g.total_vptrs + 1), stream), "memset vptr");
+    CK(launch_vgroups(g.th, d_tables, 0, stream), "vgroups count");
+    CK(launch_scan_i32(reinterpret_cast<int32_t *>(tb + g.th.vptr_off), g.total_vptrs + 1, sb + g.sc_scan, stream),
+       "scan vptr");
+    CK(launch_vgroups(g.th, d_tables, 1, stream), "vgroups scatter");
     return WASABI_OK;
 }
 
@@ -362,7 +382,7 @@ wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables
     if (!d_tables || !d_bins || (!d_psi && row1 > row0)) return fail(WASABI_EINVAL, "NULL buffer");
     if (!aligned(d_psi, 16)) return fail(WASABI_EINVAL, "d_psi must be 16-byte aligned");
     const int T = params->tile;
-    CK(launch_superpose(d_bins, d_tables, T, T + 1, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
+    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
                         row0, params->n_h, reinterpret_cast<float2 *>(d_psi), 0, nullptr, params->pitch_m, nullptr,
                         stream),
        "superpose");
@@ -381,7 +401,7 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
     double p4[4];
     if (print) { p4[0] = print->x_r_m; p4[1] = print->y_r_m; p4[2] = print->z_r_m; p4[3] = 1.0 / params->wavelength_m; }
     const int T = params->tile;
-    CK(launch_superpose(d_bins, d_tables, T, T + 1, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
+    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
                         row0, params->n_h, reinterpret_cast<float2 *>(d_u), 1, print ? p4 : nullptr, params->pitch_m,
                         d_bits, stream),
        "superpose_inverse");

@@ -20,6 +20,7 @@ ap.add_argument("--rows", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tile", type=int, default=None)
 ap.add_argument("--pkg", default=None)
+ap.add_argument("--dump", default=None, help="np.save psi (after the timed superposes) to this path")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 if a.tile:
@@ -38,3 +39,9 @@ ev[1].record()
 torch.cuda.synchronize()
 st = W.bins_stats(pl.bins)
 print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} superpose {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
+if a.dump:
+    import hashlib
+    import numpy as np
+    f = pl.field.cpu().numpy()
+    np.save(a.dump, f)
+    print(f"[{a.pkg or 'tree'}] psi sha1 {hashlib.sha1(f.tobytes()).hexdigest()} -> {a.dump}")
