@@ -59,7 +59,7 @@ def oracle_sample(cfg, pts, window=None, table_depths=None, setup=None):
         setup = {}
         geo = O.geometry(P)
         setup["area"] = [(2 * int(h)) ** 2 for h in geo["H"]]
-        w = window or min(cfg.n_h, 2048)
+        w = window or min(cfg.n_h, 4096)
         x0 = y0 = cfg.n_h // 2 - w // 2
         ix, iy, iz, ok = O.points(P, pts)
         E = geo["E"][iz]
@@ -258,11 +258,18 @@ def run_ours(args, cfg):
            "bin": 16.0 * n + 16.0 * st["n_valid"] + 8.0 * st["entries"],
            "tables": 0.0}
     dom = max(stage_ms, key=stage_ms.get)
-    traffic = None
+    # per-launch DRAM traffic and on-chip limiter of the dominant kernel, from one committed
+    # `ncu --set full` capture of this same workload (tools/ncu_traffic.py -> profiles/ncu_traffic.json)
+    traffic, onchip = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            rec = json.load(open(tpath)).get(dom)
+            if isinstance(rec, dict):
+                traffic = rec.get("traffic")
+                onchip = rec.get("onchip")
+            else:
+                traffic = rec
         except Exception:
             traffic = None
     ach = alg[dom] / (stage_ms[dom] * 1e-3) / 1e9 if alg[dom] else 0.0
@@ -271,6 +278,8 @@ def run_ours(args, cfg):
                 "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
                 "step_achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,
                 "step_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
+    if onchip:
+        roofline["onchip"] = onchip
 
     # end-to-end through the C ABI with host buffers (H2D points + whole path + D2H bits)
     e2e = None

@@ -66,8 +66,19 @@ typedef struct {
     double retention;     /* r in (0, 1]: N_r,d = min(nnz_d, ceil(r_ppm nnz_d / 1e6)), r_ppm =
                              llround(r 1e6) >= 1 (R-A4; the paper's N_r = pi (W/2)^2 gamma, :92)   */
     int32_t tile;         /* T: bin / superposition tile side; 64 or 128 (multiple of 2^L)        */
-    uint32_t flags;       /* reserved, must be 0                                                    */
+    uint32_t flags;       /* 0, or WASABI_FLAG_EXACT_SHIFT; other bits: EINVAL                      */
 } wasabi_params;
+
+/* Exact off-grid shifts (reading R-A20; needs levels <= 4).  Instead of
+ * one table per depth whose level-l coefficients are shifted by s_l = 2^l floor((i + 2^(l-1))/2^l)
+ * (R-A8, exact only for 2^L-aligned points), every depth d gets 4^L "offset-class" tables
+ * t = d 4^L + cy 2^L + cx, (cx, cy) = (ix, iy) mod 2^L, each the PSF centred at (H + cx, H + cy)
+ * in a (2H + 2^L)^2 table, transformed and shrunk on its own; every coefficient of a point is
+ * shifted by the 2^L-aligned (ix - cx, iy - cy).  At r = 1 the hologram then equals the
+ * quantised direct sum for ANY integer position.  In this mode the `depth` argument of
+ * wasabi_depth_geometry / wasabi_export_table / wasabi_export_reach is the table index t
+ * (0 <= t < wasabi_table_count). */
+#define WASABI_FLAG_EXACT_SHIFT 1u
 
 /* Spherical reference wave point (paper default (0, 0.030, -0.400) m). */
 typedef struct {
@@ -98,8 +109,11 @@ wasabi_status wasabi_psf_tables_bytes(const wasabi_params *params, size_t *table
 wasabi_status wasabi_build_psf_tables(const wasabi_params *params, void *d_tables, size_t table_bytes,
                                       void *d_scratch, size_t scratch_bytes, cudaStream_t stream);
 
-/* Geometry of depth `depth` (host only). */
+/* Geometry of depth `depth` (host only; table index in WASABI_FLAG_EXACT_SHIFT mode). */
 wasabi_status wasabi_depth_geometry(const wasabi_params *params, int32_t depth, wasabi_depth_info *out);
+
+/* Number of PSF tables: n_depth, or n_depth 4^L with WASABI_FLAG_EXACT_SHIFT (host only). */
+wasabi_status wasabi_table_count(const wasabi_params *params, int64_t *n_tables);
 
 /* ---------------------------------------------------------------- step 2a */
 

@@ -17,6 +17,9 @@ LIB_PATH = os.path.join(_HERE, "libwasabi.so")
 WASABI_OK, WASABI_EINVAL, WASABI_ENOSPC, WASABI_ECUDA, WASABI_ESTATE = 0, -1, -2, -3, -4
 
 
+FLAG_EXACT_SHIFT = 1   # include/wasabi.h WASABI_FLAG_EXACT_SHIFT
+
+
 class WasabiError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"wasabi status {status}: {msg}")
@@ -51,6 +54,7 @@ class Params:
     z_max: float
     retention: float
     tile: int = 64
+    exact: bool = False   # WASABI_FLAG_EXACT_SHIFT: offset-class tables (R-A20)
 
     @staticmethod
     def from_config(cfg, **kw) -> "Params":
@@ -60,7 +64,7 @@ class Params:
 
     def c(self) -> _CParams:
         return _CParams(self.wavelength, self.pitch, self.n_h, self.n_depth, self.levels, self.z_min,
-                        self.z_max, self.retention, self.tile, 0)
+                        self.z_max, self.retention, self.tile, FLAG_EXACT_SHIFT if self.exact else 0)
 
 
 @dataclasses.dataclass(frozen=True)
@@ -97,6 +101,7 @@ def lib() -> C.CDLL:
             "wasabi_psf_tables_bytes": [_PP, C.POINTER(_sz), C.POINTER(_sz)],
             "wasabi_build_psf_tables": [_PP, _vp, _sz, _vp, _sz, _vp],
             "wasabi_depth_geometry": [_PP, C.c_int32, C.POINTER(_CDepthInfo)],
+            "wasabi_table_count": [_PP, C.POINTER(_i64)],
             "wasabi_bin_points_bytes": [_PP, _i64, _i64, _i64, C.POINTER(_sz)],
             "wasabi_bin_points": [_PP, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp],
             "wasabi_superpose": [_PP, _vp, _vp, _i64, _i64, _vp, _vp],
@@ -173,6 +178,12 @@ def depth_geometry(p: Params, depth: int) -> dict:
     o = _CDepthInfo()
     _check(lib().wasabi_depth_geometry(C.byref(p.c()), depth, C.byref(o)))
     return dict(z=o.z_m, R=o.radius_px, H=o.half, E=o.footprint, nnz=o.nnz, n_r=o.n_r)
+
+
+def table_count(p: Params) -> int:
+    n = _i64()
+    _check(lib().wasabi_table_count(C.byref(p.c()), C.byref(n)))
+    return int(n.value)
 
 
 # ----------------------------------------------------------------------------- step 2a

@@ -18,16 +18,26 @@ __host__ __device__ inline uint32_t pack_entry_pos(int X, int Y, int level) {
     return (uint32_t)X | ((uint32_t)Y << 14) | ((uint32_t)level << 28);
 }
 
-// Compact per-depth data read by the hot kernels (64 bytes).
+// Compact per-table data read by the hot kernels (72 bytes).
 struct KDesc {
-    int32_t H;                    // table half side
+    int32_t H;                    // table half side (H, vbase: one 8-byte load in the hot kernel)
+    int32_t vbase;                // window LUT pointer slots of this table start here (== vptr_base[0])
     int32_t E;                    // structural footprint bound ceil(R) + 3 2^(L-1) (buffer sizing)
     int32_t Ek;                   // kept reach, per axis (R-A19; computed by the table build)
     int32_t Q;                    // kept reach, squared distance (R-A19; computed by the table build)
     int32_t ptr_base[kMaxLevels]; // canonical LUT: level l (1..L) band pointer rows start at ptr_base[l-1]
     int32_t vptr_base[kMaxLevels];// window LUT: level l pointer rows start at vptr_base[l-1]
-    int32_t pad[2];
+    int32_t side;                 // table side: 2H, or 2H + 2^L for offset-class tables (R-A20)
 };
+static_assert(sizeof(KDesc) % 8 == 0, "KDesc: (H, vbase) is read as one 8-byte load");
+
+// Offset-class tables (WASABI_FLAG_EXACT_SHIFT, reading R-A20): with cb = L class bits, depth d
+// has 4^L tables t = (d << 2cb) | (cy << cb) | cx, (cx, cy) = (ix, iy) mod 2^L; every level of a
+// point is shifted by the 2^L-aligned (ix - cx, iy - cy).  cb = 0: one table per depth.
+__host__ __device__ inline int table_of(int ix, int iy, int iz, int cb) {
+    const int m = (1 << cb) - 1;
+    return (iz << (2 * cb)) | ((iy & m) << cb) | (ix & m);
+}
 
 // ---- window LUT (the superposition kernel's copy of the kept lists) ----
 // A warp of the superposition kernel owns a 32-row strip of a T x T tile.  For a point and a
@@ -44,11 +54,17 @@ constexpr int kWinRows = 32;
 #define WASABI_WIN_MARGIN 6
 #endif
 constexpr int kWinMargin = WASABI_WIN_MARGIN;   // >= 6 (level-1 column-group overrun)
-__host__ __device__ inline int win_lq(int l) { return l < 5 ? l : 5; }          // log2 q_l
+// log2 q_l: window starts are multiples of min(2^l, 32); with offset-class tables (cb = L class
+// bits, R-A20) every level is shifted by multiples of 2^L, so of min(2^max(l, L), 32)
+__host__ __device__ inline int win_lq(int l, int cb) { const int m = l > cb ? l : cb; return m < 5 ? m : 5; }
 __host__ __device__ inline int win_lg(int l) { return l < 3 ? 3 : l; }          // log2 G_l
-__host__ __device__ inline int win_variants(int l) { return kWinRows >> win_lq(l); }
+__host__ __device__ inline int win_variants(int l, int cb) { return kWinRows >> win_lq(l, cb); }
 __host__ __device__ inline int win_bands(int side) { return (side + kWinRows - 1) / kWinRows + 1; }
 __host__ __device__ inline int win_cols(int side, int l) { return (side + (1 << win_lg(l)) - 1) >> win_lg(l); }
+// pointer slots of level l of one table
+__host__ __device__ inline int win_slots(int side, int l, int cb) {
+    return win_variants(l, cb) * win_bands(side) * (win_cols(side, l) + 1);
+}
 
 // Per-depth data used by the table build and exports.
 struct DDesc {
@@ -61,12 +77,13 @@ struct DDesc {
     int32_t group_base; // prefix of (level, band, Xb) groups (== its ptr_base for level 1)
     int32_t n_groups;
     int32_t vgroup_base; // prefix of window-LUT pointer slots (== its vptr_base for level 1)
+    int32_t cx, cy;      // PSF centre offset from (H, H): the offset class (R-A20), else 0
 };
 
 struct TableHeader {
     uint64_t magic;
     uint64_t param_hash;
-    int32_t n_depth, levels, tile, S;  // S = smem row stride baked into packed positions
+    int32_t n_depth, levels, tile, S;  // n_depth = number of TABLES; S = smem row stride baked into positions
     int64_t total_entries;             // sum N_r,d
     int64_t total_ptrs;                // int32 pointer slots
     int64_t total_ctas;                // K1 grid
@@ -76,7 +93,8 @@ struct TableHeader {
     int64_t total_vptrs;               // window-LUT int32 pointer slots
     int64_t vent_cap;                  // window-LUT entry capacity (bound: 16 N_r per depth)
     int64_t vptr_off, vval_off, vpos_off;  // window LUT: pointers, float2 values, uint16 positions
-    int64_t pad[3];
+    int32_t cls_bits, n_zlevels;       // offset-class bits cb (0 or L) and depth levels N_z
+    int64_t pad[2];
 };
 static_assert(sizeof(TableHeader) <= 256, "table header must fit the 256-byte slot");
 
@@ -129,13 +147,14 @@ cudaError_t launch_scan_u32_to_u64(const uint32_t *in, unsigned long long *out, 
 size_t scan_scratch_bytes(int64_t n);
 
 cudaError_t launch_bin(const BinHeader &bh, void *d_bins, const KDesc *kd, const float4 *pts,
-                       double pitch, int64_t n_h, double z_min, double dz, int n_depth, cudaStream_t s);
+                       double pitch, int64_t n_h, double z_min, double dz, int n_depth, int cls_bits,
+                       cudaStream_t s);
 
 // fused = 0: write psi; fused = 1: inverse Haar in shared memory, write u (psi pointer, may be NULL)
 // and, if bits != NULL, the print bits (print4 = {xr, yr, zr, 1/lambda}).
-cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x, int tiles_y,
-                             int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
-                             uint8_t *bits, cudaStream_t s);
+cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int cls_bits, int tiles_x,
+                             int tiles_y, int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4,
+                             double pitch, uint8_t *bits, cudaStream_t s);
 cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStream_t s);
 
 cudaError_t launch_psf_dense(const DenseDesc *d_desc, int n_depth, float2 *out, double k, double pitch,

@@ -21,7 +21,7 @@ __device__ __forceinline__ long long floor_div(long long a, long long b) {
 struct BinArgs {
     int64_t n;
     int64_t n_h, row0, row1;
-    int T, tiles_x, tiles_y, n_depth;
+    int T, tiles_x, tiles_y, n_depth, cls_bits;
     double pitch, z_min, dz;
 };
 
@@ -74,8 +74,9 @@ __global__ void __launch_bounds__(256) convert_count_kernel(const float4 *__rest
         pout[j] = make_int4(ix, iy, valid ? iz : -1, __float_as_int(p.w));
         if (valid) {
             int tx0, tx1, ty0, ty1;
-            const int Q = kd[iz].Q;
-            tile_range(ix, iy, kd[iz].Ek, A, tx0, tx1, ty0, ty1);
+            const int tb = table_of(ix, iy, iz, A.cls_bits);
+            const int Q = kd[tb].Q;
+            tile_range(ix, iy, kd[tb].Ek, A, tx0, tx1, ty0, ty1);
             for (int ty = ty0; ty <= ty1; ty++) {
                 const int rem = Q - sq_gap(iy, (int)A.row0 + ty * A.T, A.T);
                 if (rem < 0) continue;
@@ -101,8 +102,9 @@ __global__ void __launch_bounds__(256) scatter_kernel(BinArgs A, const KDesc *__
     const int4 q = pconv[j];
     if (q.z < 0) return;
     int tx0, tx1, ty0, ty1;
-    const int Q = kd[q.z].Q;
-    tile_range(q.x, q.y, kd[q.z].Ek, A, tx0, tx1, ty0, ty1);
+    const int tb = table_of(q.x, q.y, q.z, A.cls_bits);
+    const int Q = kd[tb].Q;
+    tile_range(q.x, q.y, kd[tb].Ek, A, tx0, tx1, ty0, ty1);
     for (int ty = ty0; ty <= ty1; ty++) {
         const int rem = Q - sq_gap(q.y, (int)A.row0 + ty * A.T, A.T);
         if (rem < 0) continue;
@@ -219,7 +221,7 @@ __global__ void finish_kernel(BinHeader *bh, const unsigned long long *ptr, int6
 }  // namespace
 
 cudaError_t launch_bin(const BinHeader &h, void *d_bins, const KDesc *kd, const float4 *pts, double pitch,
-                       int64_t n_h, double z_min, double dz, int n_depth, cudaStream_t s) {
+                       int64_t n_h, double z_min, double dz, int n_depth, int cls_bits, cudaStream_t s) {
     char *base = reinterpret_cast<char *>(d_bins);
     BinHeader *bh = reinterpret_cast<BinHeader *>(base);
     int4 *pconv = reinterpret_cast<int4 *>(base + h.pts_off);
@@ -234,7 +236,7 @@ cudaError_t launch_bin(const BinHeader &h, void *d_bins, const KDesc *kd, const 
 
     BinArgs A;
     A.n = h.n_points; A.n_h = n_h; A.row0 = h.row0; A.row1 = h.row1;
-    A.T = h.T; A.tiles_x = h.tiles_x; A.tiles_y = h.tiles_y; A.n_depth = n_depth;
+    A.T = h.T; A.tiles_x = h.tiles_x; A.tiles_y = h.tiles_y; A.n_depth = n_depth; A.cls_bits = cls_bits;
     A.pitch = pitch; A.z_min = z_min; A.dz = dz;
     cudaError_t e;
     if ((e = cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(h.n_tiles + 1), s)) != cudaSuccess) return e;

@@ -27,7 +27,7 @@ namespace wasabi {
 namespace {
 
 struct SupArgs {
-    int L, tiles_x;
+    int L, cls_bits, tiles_x;
     int64_t row0, n_h;
 };
 
@@ -40,7 +40,21 @@ struct SupArgs {
 #ifndef WASABI_PF
 #define WASABI_PF 1
 #endif
-constexpr int kD = WASABI_KD;          // register ring depth (chunks in flight per warp)
+#ifndef WASABI_PRED_IDLE
+#define WASABI_PRED_IDLE 0
+#endif
+constexpr int kD = WASABI_KD;          // chunks per group (two groups in flight per warp)
+
+// Predicated read-only loads: the destination keeps its previous value when c is false, and the
+// load never forces a wait on its result (the selects happen in the consumer).
+__device__ __forceinline__ void ldg_v2_if(float2 &v, const float2 *p, bool c) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.nc.v2.f32 {%0, %1}, [%2];\n\t}"
+                 : "+f"(v.x), "+f"(v.y) : "l"(p), "r"((int)c));
+}
+__device__ __forceinline__ void ldg_u16_if(int &v, const uint16_t *p, bool c) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u16 %0, [%1];\n\t}"
+                 : "+r"(v) : "l"(p), "r"((int)c));
+}
 
 // Bulk prefetch of [p, p + bytes) into L2 (16-byte granules): one instruction per range, so the
 // later chunks of a range hit L2 instead of waiting on DRAM.
@@ -107,21 +121,24 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     float a_l = 0.f;
     int beg[4], len[4], base[4];
     unsigned msk[4];
-    auto range = [&](int l, int ix, int iy, int H, int d, bool ok, int &b, int &n, int &bs) {
+    const int cmask = (1 << A.cls_bits) - 1;
+    auto range = [&](int l, int ix, int iy, int H, int side, int vrow, bool ok, int &b, int &n, int &bs) {
         b = 0; n = 0; bs = 0;
         if (l == 0) return;
-        const int h = 1 << (l - 1), side = 2 * H;
-        const int sx = ((ix + h) >> l) << l, sy = ((iy + h) >> l) << l;
+        const int h = 1 << (l - 1);
+        // R-A8 level shift, or the 2^L-aligned shift of the offset-class tables (R-A20)
+        const int sx = cmask ? ix & ~cmask : ((ix + h) >> l) << l;
+        const int sy = cmask ? iy & ~cmask : ((iy + h) >> l) << l;
         const int o = strip_y0 - sy + H;                 // window rows [o, o + 32)
         const int xs = tile_x0 - sx + H;                 // window columns [xs, xs + T)
         ok = ok && o > -kWinRows && o < side && xs > -T && xs < side;
-        const int lq = win_lq(l), lg = win_lg(l);
+        const int lq = win_lq(l, A.cls_bits), lg = win_lg(l);
         const int v = (o & (kWinRows - 1)) >> lq;
         const int k = (o - (v << lq) + kWinRows) >> 5;
         const int ncol = win_cols(side, l);
         const int xa = max(xs >> lg, 0), xb = min((xs + T + (1 << lg) - 1) >> lg, ncol);
         if (ok && xa < xb) {
-            const int row = __ldg(&kd[d].vptr_base[l - 1]) + (v * win_bands(side) + k) * (ncol + 1);
+            const int row = vrow + (v * win_bands(side) + k) * (ncol + 1);
             b = __ldg(vptr + row + xa);
             n = __ldg(vptr + row + xb) - b;
         }
@@ -132,17 +149,29 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             const int nq = (int)min((unsigned long long)32, b1 - pb);
             const bool ok = lane < nq;
             int4 q = make_int4(0, 0, 0, 0);
-            int H = 0;
+            int2 hv = make_int2(0, 0);          // (H, first window-LUT pointer slot)
             if (ok) {
                 q = __ldg(pconv + __ldg(bidx + pb + lane));
-                H = __ldg(&kd[q.z].H);
+                hv = __ldg(reinterpret_cast<const int2 *>(&kd[table_of(q.x, q.y, q.z, A.cls_bits)].H));
             }
             pb += nq;
             a_l = __int_as_float(q.w);
-            range(lv0, q.x, q.y, H, q.z, ok, beg[0], len[0], base[0]);
-            range(lv1, q.x, q.y, H, q.z, ok, beg[1], len[1], base[1]);
-            range(lv2, q.x, q.y, H, q.z, ok, beg[2], len[2], base[2]);
-            range(lv3, q.x, q.y, H, q.z, ok, beg[3], len[3], base[3]);
+            const int side = 2 * hv.x + (A.cls_bits ? 1 << A.L : 0);
+            // pointer rows of the class's levels: level l starts after the slots of levels < l
+            int vr[4];
+            {
+                int acc = hv.y, l = 1;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int lj = j == 0 ? lv0 : j == 1 ? lv1 : j == 2 ? lv2 : lv3;
+                    for (; l < lj; l++) acc += win_slots(side, l, A.cls_bits);
+                    vr[j] = acc;
+                }
+            }
+            range(lv0, q.x, q.y, hv.x, side, vr[0], ok, beg[0], len[0], base[0]);
+            range(lv1, q.x, q.y, hv.x, side, vr[1], ok, beg[1], len[1], base[1]);
+            range(lv2, q.x, q.y, hv.x, side, vr[2], ok, beg[2], len[2], base[2]);
+            range(lv3, q.x, q.y, hv.x, side, vr[3], ok, beg[3], len[3], base[3]);
             bool any = false;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -160,8 +189,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         return false;
     };
 
-    // chunk generator (warp-uniform): level slot gj, remaining points gm, current range
-    int gj = 0, c_beg = 0, c_end = 0;
+    // range generator (warp-uniform): level slot gj, remaining points gm, current range
+    int gj = 0, c_beg = 0, c_end = 0, c_dpos = 0;
     uint32_t c_sa = 0u;
     unsigned gm = 0u;
     float c_a = 0.f;
@@ -185,7 +214,9 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         gm &= gm - 1u;
         c_beg = __shfl_sync(kFull, s_beg, p);
         c_end = c_beg + __shfl_sync(kFull, s_len, p);
-        c_sa = tile_sa + 8u * (uint32_t)__shfl_sync(kFull, s_base, p);
+        const int bse = __shfl_sync(kFull, s_base, p);
+        c_sa = tile_sa + 8u * (uint32_t)bse;
+        c_dpos = dummy - bse;                 // position that maps an idle lane to its dummy cell
         c_a = __shfl_sync(kFull, a_l, p);
         have = true;
     };
@@ -195,51 +226,58 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         next_range();
     }
 
-    // ring slot: value, position, smem byte base of the range (dummy cell for idle lanes), a_j;
-    // an idle lane's value is stale but finite-or-not, it only ever reaches its dummy cell
-    const uint32_t dummy_sa = tile_sa + 8u * (uint32_t)dummy;
-    float2 rv[kD];
-    int rp[kD];
-    uint32_t rb[kD];
-    float ra[kD];
+    // Groups of up to kG chunks of one range, double-buffered (A, B): the loads of the next group
+    // are issued before the current group is consumed.  Idle lanes carry a position that points
+    // at the warp's dummy cell (their stale value only ever reaches it).
+    constexpr int kG = kD;
+    float2 va[kG], vb[kG];
+    int pa[kG], pb_[kG];
+    uint32_t saA = 0u, saB = 0u;
+    float aA = 0.f, aB = 0.f;
+    int nA = 0, nB = 0, dA = 0, dB = 0;
 #pragma unroll
-    for (int s = 0; s < kD; s++) rv[s] = make_float2(0.f, 0.f);
-#define WASABI_PREFETCH(s)                                                          \
+    for (int u = 0; u < kG; u++) { va[u] = make_float2(0.f, 0.f); vb[u] = va[u]; pa[u] = 0; pb_[u] = 0; }
+#define WASABI_FILL(V, P, SA, AA, N, DP)                                            \
     do {                                                                            \
-        const int e = c_beg + lane;                                                 \
-        const bool v = have && e < c_end;                                           \
-        rp[s] = 0;                                                                  \
-        if (v) {                                                                    \
-            rv[s] = __ldg(vval + e);                                                \
-            rp[s] = __ldg(vpos + e);                                                \
-        }                                                                           \
-        rb[s] = v ? c_sa : dummy_sa;                                                \
-        ra[s] = c_a;                                                                \
+        N = 0;                                                                      \
         if (have) {                                                                 \
-            c_beg += 32;                                                            \
+            SA = c_sa; AA = c_a; DP = c_dpos;                                       \
+            N = min(kG, (c_end - c_beg + 31) >> 5);                                 \
+            const int e0 = c_beg + lane, last = c_end - 1 - e0;                     \
+            const float2 *vp = vval + e0;                                           \
+            const uint16_t *pp = vpos + e0;                                         \
+            _Pragma("unroll") for (int u = 0; u < kG; u++) {                        \
+                /* values: whole chunks (the LUT is padded); positions: idle lanes keep \
+                   the dummy position */                                            \
+                ldg_v2_if(V[u], vp + 32 * u, u < N);                                \
+                P[u] = c_dpos;                                                      \
+                ldg_u16_if(P[u], pp + 32 * u, u < N && 32 * u <= last);            \
+            }                                                                       \
+            c_beg += 32 * N;                                                        \
             if (c_beg >= c_end) next_range();                                       \
         }                                                                           \
     } while (0)
-#define WASABI_CONSUME(s)                                                           \
+#define WASABI_CONSUME(V, P, SA, AA, N, DP)                                         \
     do {                                                                            \
-        const uint32_t sa = rb[s] + 8u * (uint32_t)rp[s];                           \
-        float2 o = lds2(sa);                                                        \
-        o.x = fmaf(ra[s], rv[s].x, o.x);                                            \
-        o.y = fmaf(ra[s], rv[s].y, o.y);                                            \
-        sts2(sa, o);                                                                \
+        _Pragma("unroll") for (int u = 0; u < kG; u++) {                            \
+            if (u < N && (!WASABI_PRED_IDLE || P[u] != DP)) {                       \
+                const uint32_t sa = SA + 8u * (uint32_t)P[u];                       \
+                float2 o = lds2(sa);                                                \
+                o.x = fmaf(AA, V[u].x, o.x);                                        \
+                o.y = fmaf(AA, V[u].y, o.y);                                        \
+                sts2(sa, o);                                                        \
+            }                                                                       \
+        }                                                                           \
     } while (0)
-#pragma unroll
-    for (int s = 0; s < kD; s++) WASABI_PREFETCH(s);
-    bool more = true;
-    while (more) {
-        more = have;
-#pragma unroll
-        for (int s = 0; s < kD; s++) {
-            WASABI_CONSUME(s);
-            WASABI_PREFETCH(s);
-        }
+    WASABI_FILL(va, pa, saA, aA, nA, dA);
+    while (nA > 0) {
+        WASABI_FILL(vb, pb_, saB, aB, nB, dB);
+        WASABI_CONSUME(va, pa, saA, aA, nA, dA);
+        if (nB == 0) break;
+        WASABI_FILL(va, pa, saA, aA, nA, dA);
+        WASABI_CONSUME(vb, pb_, saB, aB, nB, dB);
     }
-#undef WASABI_PREFETCH
+#undef WASABI_FILL
 #undef WASABI_CONSUME
     __syncthreads();
     float2 *data = tile + M;                    // row r, column x at data[r * S + x]
@@ -284,12 +322,12 @@ cudaError_t launch_t(const void *d_bins, const void *d_tables, const SupArgs &A,
 
 }  // namespace
 
-cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int tiles_x, int tiles_y,
-                             int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
-                             uint8_t *bits, cudaStream_t s) {
+cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int cls_bits, int tiles_x,
+                             int tiles_y, int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4,
+                             double pitch, uint8_t *bits, cudaStream_t s) {
     if (S != T + kWinMargin) return cudaErrorInvalidValue;
     SupArgs A;
-    A.L = L; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
+    A.L = L; A.cls_bits = cls_bits; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
     const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
     const QArgs qa = make_qargs(print4, pitch, n_h);
     return T <= 64 ? launch_t<64>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s)

@@ -23,7 +23,11 @@ __device__ __forceinline__ T *atw(void *t, int64_t off) {
     return reinterpret_cast<T *>(reinterpret_cast<char *>(t) + off);
 }
 
-// CTA -> depth: largest d with cta_base[d] <= b (cta_base has n_depth + 1 entries).
+__device__ __forceinline__ int kdh(const void *t, int d) {
+    return at<KDesc>(t, hdr(t).kdesc_off)[d].H;
+}
+
+// CTA -> table: largest d with cta_base[d] <= b (cta_base has n_tables + 1 entries).
 __device__ __forceinline__ int find_depth(const int32_t *base, int n, int64_t b) {
     int lo = 0, hi = n;  // invariant base[lo] <= b < base[hi]
     while (hi - lo > 1) {
@@ -51,7 +55,8 @@ __global__ void __launch_bounds__(256) psf_haar_kernel(const void *tables, float
     const DDesc D = dd[d];
     const int local = (int)blockIdx.x - D.cta_base;
     const int X0 = (local % D.tiles) * kTile, Y0 = (local / D.tiles) * kTile;
-    const int side = D.side, H = side >> 1;
+    const int side = D.side;
+    const int Cx = kdh(tables, d) + D.cx, Cy = kdh(tables, d) + D.cy;   // PSF centre (R-A20: offset class)
     const double R2 = __dmul_rn(D.R, D.R);
     const double z2 = __dmul_rn(D.z, D.z);
 
@@ -60,7 +65,7 @@ __global__ void __launch_bounds__(256) psf_haar_kernel(const void *tables, float
         const int X = X0 + x, Y = Y0 + y;
         double2 v = make_double2(0.0, 0.0);
         if (X < side && Y < side) {
-            const long long dx = X - H, dy = Y - H;
+            const long long dx = X - Cx, dy = Y - Cy;
             const bool in = (dx == 0 && dy == 0) || ((double)(dx * dx + dy * dy) < R2);
             if (in) {
                 const double xp = __dmul_rn((double)dx, pitch), yp = __dmul_rn((double)dy, pitch);
@@ -222,8 +227,11 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
                             ent[out] = make_uint4(pack_entry_pos(X, Y, l), __float_as_uint(v.x), __float_as_uint(v.y), 0u);
                             out++;
                         } else {
-                            // target within |dX| + 2^(l-1) of the point per axis (s_l(i) - i in (-h, h])
-                            const int ax = abs(X - K.H) + st_px, ay = abs(Y - K.H) + st_px;
+                            // target within |dX| + 2^(l-1) of the point per axis (s_l(i) - i in (-h, h]);
+                            // offset-class tables: exactly (dX - cx, dY - cy) from the point (R-A20)
+                            const bool ex = h.cls_bits != 0;
+                            const int ax = ex ? abs(X - K.H - D.cx) : abs(X - K.H) + st_px;
+                            const int ay = ex ? abs(Y - K.H - D.cy) : abs(Y - K.H) + st_px;
                             ek = max(ek, max(ax, ay));
                             q = max(q, ax * ax + ay * ay);
                         }
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(256) vgroups_kernel(void *tables, int n_depth,
     }
     const int row = (int)(local / (ncol + 1));
     const int v = row / nband, k = row % nband;
-    const int bs = (v << win_lq(l)) + kWinRows * (k - 1);
+    const int bs = (v << win_lq(l, h.cls_bits)) + kWinRows * (k - 1);
     const int y0 = max(bs, 0), y1 = min(bs + kWinRows, side);
     const int lg = win_lg(l);
     const int nb = side >> l, bh = band_blocks(T, l) << l;              // canonical band height (px)

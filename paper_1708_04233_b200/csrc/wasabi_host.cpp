@@ -60,6 +60,7 @@ uint64_t param_hash(const wasabi_params &P) {
     h = fnv(h, &P.wavelength_m, 8); h = fnv(h, &P.pitch_m, 8); h = fnv(h, &P.n_h, 8);
     h = fnv(h, &P.n_depth, 4); h = fnv(h, &P.levels, 4); h = fnv(h, &P.z_min_m, 8);
     h = fnv(h, &P.z_max_m, 8); h = fnv(h, &P.retention, 8); h = fnv(h, &P.tile, 4);
+    h = fnv(h, &P.flags, 4);
     return h;
 }
 
@@ -81,7 +82,9 @@ wasabi_status validate(const wasabi_params *P) {
     if (P->n_depth > 1 && !(P->z_max_m > P->z_min_m)) return fail(WASABI_EINVAL, "n_depth > 1 needs z_max > z_min");
     if (!(P->retention > 0) || P->retention > 1) return fail(WASABI_EINVAL, "retention must be in (0, 1]");
     if (llround(P->retention * 1e6) < 1) return fail(WASABI_EINVAL, "retention below 1 ppm");
-    if (P->flags != 0) return fail(WASABI_EINVAL, "flags must be 0");
+    if (P->flags & ~(uint32_t)WASABI_FLAG_EXACT_SHIFT) return fail(WASABI_EINVAL, "unknown flags 0x%x", P->flags);
+    if ((P->flags & WASABI_FLAG_EXACT_SHIFT) && P->levels > 4)
+        return fail(WASABI_EINVAL, "WASABI_FLAG_EXACT_SHIFT needs levels <= 4 (4^L offset-class tables per depth)");
     return WASABI_OK;
 }
 
@@ -98,14 +101,13 @@ inline bool in_support(int64_t dx, int64_t dy, double R) {
     return (double)(dx * dx + dy * dy) < R * R;
 }
 
-// Structural nnz: coefficient positions whose support block touches S_d.  Per block row the
-// disc's x-extent is the union of symmetric row intervals [-xm, xm], so the blocks touched are
-// those overlapping [H - max xm, H + max xm].
-int64_t nnz_structural(int64_t H, double R, int L) {
-    const int64_t side = 2 * H;
+// Structural nnz: coefficient positions whose support block touches S_d (centre (Cx, Cy) in a
+// side x side table).  Per block row the disc's x-extent is the union of symmetric row intervals
+// [-xm, xm], so the blocks touched are those overlapping [Cx - max xm, Cx + max xm].
+int64_t nnz_structural(int64_t side, int64_t Cx, int64_t Cy, double R, int L) {
     std::vector<int64_t> xm(side);
     for (int64_t Y = 0; Y < side; Y++) {
-        const int64_t dy = Y - H;
+        const int64_t dy = Y - Cy;
         const double s = R * R - (double)(dy * dy);
         int64_t x = s > 0 ? (int64_t)std::floor(std::sqrt(s)) : 0;
         while (x >= 0 && !in_support(x, dy, R)) x--;
@@ -119,7 +121,7 @@ int64_t nnz_structural(int64_t H, double R, int L) {
             int64_t X = -1;
             for (int64_t Y = Y0; Y < Y0 + b; Y++) X = std::max(X, xm[Y]);
             if (X < 0) continue;
-            const int64_t nblk = (H + X) / b - (H - X) / b + 1;
+            const int64_t nblk = (Cx + X) / b - (Cx - X) / b + 1;
             nnz += nblk * (l == L ? 4 : 3);
         }
     }
@@ -129,7 +131,7 @@ int64_t nnz_structural(int64_t H, double R, int L) {
 struct Geo {
     wasabi_params P;
     double k, tan_theta, dz;
-    int T, S, L, nd;
+    int T, S, L, nd, nz, cb;   // nd = tables, nz = depth levels, cb = offset-class bits (R-A20)
     std::vector<KDesc> kd;
     std::vector<DDesc> dd;
     std::vector<int32_t> ctabase;
@@ -148,7 +150,9 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     wasabi_status st = validate(P);
     if (st != WASABI_OK) return st;
     g.P = *P;
-    g.T = P->tile; g.S = P->tile + kWinMargin; g.L = P->levels; g.nd = P->n_depth;
+    g.T = P->tile; g.S = P->tile + kWinMargin; g.L = P->levels; g.nz = P->n_depth;
+    g.cb = (P->flags & WASABI_FLAG_EXACT_SHIFT) ? P->levels : 0;
+    g.nd = P->n_depth << (2 * g.cb);
     g.k = 2.0 * kPi / P->wavelength_m;
     const double sigma = P->wavelength_m / (2.0 * P->pitch_m);
     g.tan_theta = sigma / std::sqrt(1.0 - sigma * sigma);
@@ -159,29 +163,34 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     const int64_t B = 1ll << g.L;
     int64_t ptr = 0, ctas = 0, coef = 0, entries = 0, vptr = 0;
     for (int d = 0; d < g.nd; d++) {
-        const double z = level_z(*P, g.dz, d);
+        const int zi = d >> (2 * g.cb);                      // depth level of table d
+        const int cx = d & ((1 << g.cb) - 1), cy = (d >> g.cb) & ((1 << g.cb) - 1);
+        const double z = level_z(*P, g.dz, zi);
         const double R = std::fabs(z) * g.tan_theta / P->pitch_m;
         const int64_t H = B * ((int64_t)std::floor(R / (double)B) + 1);
-        if (2 * H > kMaxTableSide)
-            return fail(WASABI_EINVAL, "depth %d: PSF table side %lld exceeds %d (|z| too large for this pitch)", d,
-                        (long long)(2 * H), kMaxTableSide);
+        const int64_t side = 2 * H + (g.cb ? B : 0);
+        if (side > kMaxTableSide)
+            return fail(WASABI_EINVAL, "depth %d: PSF table side %lld exceeds %d (|z| too large for this pitch)", zi,
+                        (long long)side, kMaxTableSide);
         const int64_t E = (int64_t)std::ceil(R) + 3 * (1ll << (g.L - 1));
         DDesc &D = g.dd[d];
         KDesc &K = g.kd[d];
         D.z = z; D.R = R;
-        D.side = (int32_t)(2 * H);
-        D.tiles = (int32_t)((2 * H + 63) / 64);
+        D.side = (int32_t)side;
+        D.cx = cx; D.cy = cy;
+        K.side = (int32_t)side;
+        D.tiles = (int32_t)((side + 63) / 64);
         D.cta_base = (int32_t)ctas;
         g.ctabase[d] = (int32_t)ctas;
         ctas += (int64_t)D.tiles * D.tiles;
         D.coef_off = coef;
-        coef += 4 * H * H;
+        coef += side * side;
         K.H = (int32_t)H;
         K.E = (int32_t)E;
         g.max_E = std::max(g.max_E, E);
         D.group_base = (int32_t)ptr;
         for (int l = 1; l <= g.L; l++) {
-            const int64_t nb = (2 * H) >> l, hb = band_blocks(g.T, l), nbands = (nb + hb - 1) / hb;
+            const int64_t nb = side >> l, hb = band_blocks(g.T, l), nbands = (nb + hb - 1) / hb;
             K.ptr_base[l - 1] = (int32_t)ptr;
             ptr += nbands * (nb + 1);
         }
@@ -189,20 +198,21 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
         D.n_groups = (int32_t)(ptr - D.group_base);
         // window LUT pointer rows: per level, variants x bands x (column groups + 1)
         D.vgroup_base = (int32_t)vptr;
+        K.vbase = (int32_t)vptr;
         for (int l = 1; l <= g.L; l++) {
             K.vptr_base[l - 1] = (int32_t)vptr;
-            vptr += (int64_t)win_variants(l) * win_bands(D.side) * (win_cols(D.side, l) + 1);
+            vptr += win_slots(D.side, l, g.cb);
         }
         for (int l = g.L + 1; l <= kMaxLevels; l++) K.vptr_base[l - 1] = (int32_t)vptr;
-        D.nnz = nnz_structural(H, R, g.L);
+        D.nnz = nnz_structural(side, H + cx, H + cy, R, g.L);
         {
             const int64_t r_ppm = llround(P->retention * 1e6);
             const int64_t n = (r_ppm * D.nnz + 999999) / 1000000;
             D.n_r = std::min(n, D.nnz);
         }
         entries += D.n_r;
-        if (ptr > (int64_t)INT32_MAX / 2 || entries > (int64_t)INT32_MAX / 32 || ctas > (int64_t)INT32_MAX / 2 ||
-            vptr > (int64_t)INT32_MAX / 2)
+        if (ptr > (int64_t)INT32_MAX / 2 || entries * win_variants(1, g.cb) > (int64_t)INT32_MAX / 2 ||
+            ctas > (int64_t)INT32_MAX / 2 || vptr > (int64_t)INT32_MAX / 2)
             return fail(WASABI_EINVAL, "table too large for 32-bit indices");
     }
     g.ctabase[g.nd] = (int32_t)ctas;
@@ -213,6 +223,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     h.magic = kTableMagic;
     h.param_hash = param_hash(*P);
     h.n_depth = g.nd; h.levels = g.L; h.tile = g.T; h.S = g.S;
+    h.cls_bits = g.cb; h.n_zlevels = g.nz;
     h.total_entries = entries; h.total_ptrs = ptr; h.total_ctas = ctas;
     size_t off = 256;
     h.kdesc_off = off; off = align_up(off + sizeof(KDesc) * g.nd, 256);
@@ -220,12 +231,13 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     h.ctabase_off = off; off = align_up(off + 4 * (g.nd + 1), 256);
     h.ptr_off = off; off = align_up(off + 4 * (size_t)(ptr + 1), 256);
     h.ent_off = off; off = align_up(off + 16 * (size_t)entries, 256);
-    // window LUT: a level-l entry is stored once per variant (<= 16 copies)
+    // window LUT: a level-l entry is stored once per variant (<= win_variants(1) copies)
     h.total_vptrs = vptr;
-    h.vent_cap = 16 * entries;
+    h.vent_cap = win_variants(1, g.cb) * entries;
     h.vptr_off = off; off = align_up(off + 4 * (size_t)(vptr + 1), 256);
-    h.vval_off = off; off = align_up(off + 8 * (size_t)h.vent_cap, 256);
-    h.vpos_off = off; off = align_up(off + 2 * (size_t)h.vent_cap, 256);
+    // + 32 entries of padding: the superposition kernel reads whole 32-entry chunks past a range end
+    h.vval_off = off; off = align_up(off + 8 * (size_t)(h.vent_cap + 32), 256);
+    h.vpos_off = off; off = align_up(off + 2 * (size_t)(h.vent_cap + 32), 256);
     h.table_bytes = off;
     g.table_bytes = off;
     // build scratch
@@ -274,6 +286,8 @@ BinLayout bin_layout(const Geo &g, int64_t n, int64_t row0, int64_t row1) {
 
 bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+int cls_bits(const wasabi_params &P) { return (P.flags & WASABI_FLAG_EXACT_SHIFT) ? P.levels : 0; }
+
 }  // namespace
 
 extern "C" {
@@ -297,13 +311,21 @@ wasabi_status wasabi_depth_geometry(const wasabi_params *params, int32_t depth, 
     Geo g;
     wasabi_status st = compute_geo(params, g);
     if (st != WASABI_OK) return st;
-    if (depth < 0 || depth >= g.nd || !out) return fail(WASABI_EINVAL, "depth out of range");
+    if (depth < 0 || depth >= g.nd || !out) return fail(WASABI_EINVAL, "table index out of range");
     out->z_m = g.dd[depth].z;
     out->radius_px = g.dd[depth].R;
     out->half = g.kd[depth].H;
     out->footprint = g.kd[depth].E;
     out->nnz = g.dd[depth].nnz;
     out->n_r = g.dd[depth].n_r;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_table_count(const wasabi_params *params, int64_t *n_tables) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if (n_tables) *n_tables = g.nd;
     return WASABI_OK;
 }
 
@@ -369,7 +391,7 @@ wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_table
     CK(launch_write_blob(d_bins, &b.h, sizeof b.h, stream), "write bin header");
     const KDesc *kd = reinterpret_cast<const KDesc *>(static_cast<const char *>(d_tables) + g.th.kdesc_off);
     CK(launch_bin(b.h, d_bins, kd, reinterpret_cast<const float4 *>(d_points), params->pitch_m, params->n_h,
-                  params->z_min_m, g.dz, g.nd, stream),
+                  params->z_min_m, g.dz, g.nz, g.cb, stream),
        "bin");
     return WASABI_OK;
 }
@@ -382,7 +404,8 @@ wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables
     if (!d_tables || !d_bins || (!d_psi && row1 > row0)) return fail(WASABI_EINVAL, "NULL buffer");
     if (!aligned(d_psi, 16)) return fail(WASABI_EINVAL, "d_psi must be 16-byte aligned");
     const int T = params->tile;
-    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
+    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, cls_bits(*params), (int)(params->n_h / T),
+                        (int)((row1 - row0) / T),
                         row0, params->n_h, reinterpret_cast<float2 *>(d_psi), 0, nullptr, params->pitch_m, nullptr,
                         stream),
        "superpose");
@@ -401,7 +424,8 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
     double p4[4];
     if (print) { p4[0] = print->x_r_m; p4[1] = print->y_r_m; p4[2] = print->z_r_m; p4[3] = 1.0 / params->wavelength_m; }
     const int T = params->tile;
-    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, (int)(params->n_h / T), (int)((row1 - row0) / T),
+    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, cls_bits(*params), (int)(params->n_h / T),
+                        (int)((row1 - row0) / T),
                         row0, params->n_h, reinterpret_cast<float2 *>(d_u), 1, print ? p4 : nullptr, params->pitch_m,
                         d_bits, stream),
        "superpose_inverse");
@@ -449,18 +473,20 @@ struct DenseLayout {
     int64_t ctas = 0;
 };
 DenseLayout dense_layout(const Geo &g) {
+    // one unshrunk PSF per depth level (side 2H, centre (H, H)), whatever the table mode
     DenseLayout L;
-    L.dd.resize(g.nd);
+    L.dd.resize(g.nz);
     int64_t off = 0, ctas = 0;
-    for (int d = 0; d < g.nd; d++) {
+    for (int d = 0; d < g.nz; d++) {
         DenseDesc &D = L.dd[d];
-        D.z = g.dd[d].z; D.R = g.dd[d].R; D.side = g.dd[d].side; D.off = off; D.cta_base = (int32_t)ctas;
+        const int td = d << (2 * g.cb);
+        D.z = g.dd[td].z; D.R = g.dd[td].R; D.side = 2 * g.kd[td].H; D.off = off; D.cta_base = (int32_t)ctas;
         off += (int64_t)D.side * D.side;
         const int64_t t = (D.side + 63) / 64;
         ctas += t * t;
     }
     L.ctas = ctas;
-    L.data_off = align_up(sizeof(DenseDesc) * g.nd, 256);
+    L.data_off = align_up(sizeof(DenseDesc) * g.nz, 256);
     L.bytes = L.data_off + 8 * (size_t)off;
     return L;
 }
@@ -482,8 +508,8 @@ wasabi_status wasabi_build_psf_dense(const wasabi_params *params, void *d_dense,
     if (!d_dense || !aligned(d_dense, 256)) return fail(WASABI_EINVAL, "d_dense NULL or not 256-byte aligned");
     if (bytes < L.bytes) return fail(WASABI_ENOSPC, "dense table buffer needs %zu bytes", L.bytes);
     char *b = static_cast<char *>(d_dense);
-    CK(launch_write_blob(b, L.dd.data(), sizeof(DenseDesc) * g.nd, stream), "write dense desc");
-    CK(launch_psf_dense(reinterpret_cast<const DenseDesc *>(b), g.nd, reinterpret_cast<float2 *>(b + L.data_off), g.k,
+    CK(launch_write_blob(b, L.dd.data(), sizeof(DenseDesc) * g.nz, stream), "write dense desc");
+    CK(launch_psf_dense(reinterpret_cast<const DenseDesc *>(b), g.nz, reinterpret_cast<float2 *>(b + L.data_off), g.k,
                         params->pitch_m, L.ctas, stream),
        "psf_dense");
     return WASABI_OK;
