@@ -14,9 +14,13 @@
 // (float2 value + uint16 position) and does one read-modify-write in shared memory.  A chunk never
 // mixes points, so its targets are distinct; chunks run in point order for each level, so every
 // pixel (which belongs to exactly one level) accumulates in point order: bitwise deterministic
-// and independent of the band split (R-A11).  A kD-deep register ring keeps the entry loads of
-// the next chunks in flight across range, level and batch boundaries.  Column overrun of the
-// level-1/2 column groups lands in kWinMargin margin columns of the shared tile (never read).
+// and independent of the band split (R-A11).  Chunks are issued in groups of up to kD chunks of one
+// range, double-buffered: the (predicated, never-waited) loads of the next group are in flight
+// while the current group is consumed, and one bulk L2 prefetch per range and array is issued when
+// a batch's ranges are known.  Column overrun of the level-1/2 column groups lands in kWinMargin
+// margin columns of the shared tile (never read).  The kernel is bound by the L1TEX/LSU data pipe
+// (scattered 8-byte shared-memory read-modify-writes with random bank conflicts + the LUT loads;
+// DESIGN.md §6).
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -78,7 +82,7 @@ __device__ __forceinline__ int class_level(int c, int j, int L) {
     return l <= L ? l : 0;
 }
 
-template <int T>
+template <int T, bool EX>
 __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_kernel(const void *__restrict__ d_bins,
                                                                            const void *__restrict__ d_tables,
                                                                            SupArgs A, float2 *__restrict__ psi,
@@ -121,18 +125,19 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     float a_l = 0.f;
     int beg[4], len[4], base[4];
     unsigned msk[4];
-    const int cmask = (1 << A.cls_bits) - 1;
+    const int cb = EX ? A.L : 0;               // offset-class bits (R-A20) or 0
+    const int cmask = (1 << cb) - 1;
     auto range = [&](int l, int ix, int iy, int H, int side, int vrow, bool ok, int &b, int &n, int &bs) {
         b = 0; n = 0; bs = 0;
         if (l == 0) return;
         const int h = 1 << (l - 1);
         // R-A8 level shift, or the 2^L-aligned shift of the offset-class tables (R-A20)
-        const int sx = cmask ? ix & ~cmask : ((ix + h) >> l) << l;
-        const int sy = cmask ? iy & ~cmask : ((iy + h) >> l) << l;
+        const int sx = EX ? ix & ~cmask : ((ix + h) >> l) << l;
+        const int sy = EX ? iy & ~cmask : ((iy + h) >> l) << l;
         const int o = strip_y0 - sy + H;                 // window rows [o, o + 32)
         const int xs = tile_x0 - sx + H;                 // window columns [xs, xs + T)
         ok = ok && o > -kWinRows && o < side && xs > -T && xs < side;
-        const int lq = win_lq(l, A.cls_bits), lg = win_lg(l);
+        const int lq = win_lq(l, cb), lg = win_lg(l);
         const int v = (o & (kWinRows - 1)) >> lq;
         const int k = (o - (v << lq) + kWinRows) >> 5;
         const int ncol = win_cols(side, l);
@@ -152,11 +157,11 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             int2 hv = make_int2(0, 0);          // (H, first window-LUT pointer slot)
             if (ok) {
                 q = __ldg(pconv + __ldg(bidx + pb + lane));
-                hv = __ldg(reinterpret_cast<const int2 *>(&kd[table_of(q.x, q.y, q.z, A.cls_bits)].H));
+                hv = __ldg(reinterpret_cast<const int2 *>(&kd[table_of(q.x, q.y, q.z, cb)].H));
             }
             pb += nq;
             a_l = __int_as_float(q.w);
-            const int side = 2 * hv.x + (A.cls_bits ? 1 << A.L : 0);
+            const int side = 2 * hv.x + (EX ? 1 << A.L : 0);
             // pointer rows of the class's levels: level l starts after the slots of levels < l
             int vr[4];
             {
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     const int lj = j == 0 ? lv0 : j == 1 ? lv1 : j == 2 ? lv2 : lv3;
-                    for (; l < lj; l++) acc += win_slots(side, l, A.cls_bits);
+                    for (; l < lj; l++) acc += win_slots(side, l, cb);
                     vr[j] = acc;
                 }
             }
@@ -190,8 +195,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     };
 
     // range generator (warp-uniform): level slot gj, remaining points gm, current range
-    int gj = 0, c_beg = 0, c_end = 0, c_dpos = 0;
-    uint32_t c_sa = 0u;
+    int gj = 0, c_beg = 0, c_end = 0, c_dpos = dummy;    // (c_sa, c_dpos) address the dummy cell
+    uint32_t c_sa = tile_sa;
     unsigned gm = 0u;
     float c_a = 0.f;
     bool have = false;
@@ -306,16 +311,16 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         for (int x = lane; x < T; x += 32) out[(int64_t)y * A.n_h + x] = data[y * S + x];
 }
 
-template <int T>
+template <int T, bool EX>
 cudaError_t launch_t(const void *d_bins, const void *d_tables, const SupArgs &A, int64_t n_tiles, float2 *psi,
                      int fused, const QArgs &qa, uint8_t *bits, cudaStream_t s) {
     constexpr int M = kWinMargin, S = T + M;
     const int smem = (M + T * S + M + T / 16) * (int)sizeof(float2);
-    cudaError_t e = cudaFuncSetAttribute(superpose_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(superpose_kernel<T, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (n_tiles > 0) {
         count_launches(1);
-        superpose_kernel<T><<<(unsigned)n_tiles, 2 * T, smem, s>>>(d_bins, d_tables, A, psi, fused, qa, bits);
+        superpose_kernel<T, EX><<<(unsigned)n_tiles, 2 * T, smem, s>>>(d_bins, d_tables, A, psi, fused, qa, bits);
     }
     return cudaGetLastError();
 }
@@ -330,8 +335,11 @@ cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, in
     A.L = L; A.cls_bits = cls_bits; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
     const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
     const QArgs qa = make_qargs(print4, pitch, n_h);
-    return T <= 64 ? launch_t<64>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s)
-                   : launch_t<128>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s);
+    if (cls_bits)
+        return T <= 64 ? launch_t<64, true>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s)
+                       : launch_t<128, true>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s);
+    return T <= 64 ? launch_t<64, false>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s)
+                   : launch_t<128, false>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s);
 }
 
 }  // namespace wasabi

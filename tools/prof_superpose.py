@@ -19,6 +19,7 @@ ap.add_argument("--row0", type=int, default=32768)
 ap.add_argument("--rows", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tile", type=int, default=None)
+ap.add_argument("--fused", action="store_true", help="time superpose_inverse (fused path, as bench.py)")
 ap.add_argument("--pkg", default=None)
 ap.add_argument("--dump", default=None, help="np.save psi (after the timed superposes) to this path")
 a = ap.parse_args()
@@ -34,11 +35,14 @@ torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
 for _ in range(a.reps):
-    pl.superpose()
+    if a.fused:
+        pl.superpose_inverse()
+    else:
+        pl.superpose()
 ev[1].record()
 torch.cuda.synchronize()
 st = W.bins_stats(pl.bins)
-print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} superpose {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
+print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} {'fused' if a.fused else 'superpose'} {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
 if a.dump:
     import hashlib
     import numpy as np

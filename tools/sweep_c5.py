@@ -36,11 +36,18 @@ def main():
     ap.add_argument("--ns", default="10000,100000,1000000,10000000")
     ap.add_argument("--rs", default="0.01,0.02,0.05,0.10,0.25,1.0")
     ap.add_argument("--aligned", action="store_true")
+    ap.add_argument("--exact", action="store_true", help="offset-class tables (WASABI_FLAG_EXACT_SHIFT, R-A20)")
+    ap.add_argument("--levels", type=int, default=None)
+    ap.add_argument("--depths", type=int, default=None)
     ap.add_argument("--out", default="gpurun_out/c5_sweep.jsonl")
     a = ap.parse_args()
     base = CONFIGS["C5"]
     if a.aligned:
         base = base.replace(aligned=True)
+    if a.levels:
+        base = base.replace(levels=a.levels)
+    if a.depths:
+        base = base.replace(n_depth=a.depths)
     f = open(a.out, "w")
     for n in [int(x) for x in a.ns.split(",")]:
         pts = make_points(base, n=n)
@@ -49,21 +56,33 @@ def main():
         t_direct = None
         for r in [float(x) for x in a.rs.split(",")]:
             cfg = base.replace(retention=r)
-            p = W.Params.from_config(cfg)
+            p = W.Params.from_config(cfg, exact=a.exact)
             pl = W.Pipeline(p, n, 0, p.n_h)
             t_w = timed(lambda: pl.run(d_pts), reps=3 if n < 10_000_000 else 1)
             if u_ref is None:
+                # the reference uses standard-mode bins (whole PSF footprints at r <= 1)
+                if a.exact:
+                    ps = W.Params.from_config(cfg.replace(retention=1.0))
+                    pls = W.Pipeline(ps, n, 0, ps.n_h, want_bits=False)
+                    pls.build_tables()
+                    pls.bin(d_pts)
+                    bins_ref = pls.bins
+                else:
+                    bins_ref = pl.bins
                 dense = torch.empty(W.psf_dense_bytes(p), dtype=torch.uint8, device="cuda")
                 W.build_psf_dense(p, dense)
                 u_ref = torch.empty_like(pl.field)
-                t_direct = timed(lambda: W.direct_sum(p, dense, pl.bins, 0, p.n_h, u_ref), reps=1)
-                del dense
+                t_direct = timed(lambda: W.direct_sum(p, dense, bins_ref, 0, p.n_h, u_ref), reps=1)
+                del dense, bins_ref
+                if a.exact:
+                    del pls
             diff = (pl.field - u_ref).double()
             mse = float((diff * diff).sum(dim=-1).mean())
             peak = float((u_ref.double() ** 2).sum(dim=-1).max())
             psnr = 10 * math.log10(peak / mse) if mse > 0 else float("inf")
             st = W.bins_stats(pl.bins)
-            rec = {"n_points": n, "retention": r, "aligned": a.aligned, "wasabi_ms": t_w,
+            rec = {"n_points": n, "retention": r, "aligned": a.aligned, "exact": a.exact, "levels": cfg.levels,
+                   "n_depth": cfg.n_depth, "wasabi_ms": t_w,
                    "gpix_per_s": p.n_h ** 2 / (t_w * 1e-3) / 1e9, "points_per_s": n / (t_w * 1e-3),
                    "direct_sum_ms": t_direct, "speedup_vs_direct": t_direct / t_w, "psnr_db_vs_direct": psnr,
                    "bin_entries": st["entries"]}
