@@ -35,7 +35,7 @@ def build(force: bool = False) -> str:
 class _Params(C.Structure):
     _fields_ = [("wavelength", C.c_double), ("pitch", C.c_double), ("n_h", C.c_int64),
                 ("n_depth", C.c_int32), ("levels", C.c_int32), ("z_min", C.c_double),
-                ("z_max", C.c_double), ("retention", C.c_double), ("exact", C.c_int32), ("pad", C.c_int32)]
+                ("z_max", C.c_double), ("retention", C.c_double), ("exact", C.c_int32), ("wavelet", C.c_int32)]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -49,11 +49,12 @@ class Params:
     z_max: float
     retention: float
     exact: bool = False      # R-A20 offset-class tables
+    wavelet: int = 0         # 0 Haar (R-A1), 1 coif1 (R-A21)
 
     @staticmethod
-    def from_config(cfg, exact: bool = False) -> "Params":
+    def from_config(cfg, exact: bool = False, wavelet: int = 0) -> "Params":
         return Params(cfg.wavelength, cfg.pitch, cfg.n_h, cfg.n_depth, cfg.levels, cfg.z_min,
-                      cfg.z_max, cfg.retention, exact)
+                      cfg.z_max, cfg.retention, exact, wavelet)
 
     @property
     def n_tables(self) -> int:
@@ -68,7 +69,7 @@ class Params:
 
     def c(self) -> _Params:
         return _Params(self.wavelength, self.pitch, self.n_h, self.n_depth, self.levels, self.z_min,
-                       self.z_max, self.retention, int(self.exact), 0)
+                       self.z_max, self.retention, int(self.exact), int(self.wavelet))
 
 
 _dp = C.POINTER(C.c_double)
@@ -92,6 +93,14 @@ def lib():
             L.orc_table_coeffs.argtypes = [_pp, C.c_int64, _dp]
             L.orc_select.argtypes = [_pp, C.c_int64, _i32p, _i32p, _i32p, _dp, C.c_int64]
             L.orc_table_info.argtypes = [_pp, C.c_int64, _i64p]
+            L.orc_filter_bank.argtypes = [C.c_int, _dp, _dp, C.POINTER(C.c_int)]
+            L.orc_fb_fwd.argtypes = [C.c_int, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+            L.orc_fb_inv.argtypes = [C.c_int, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+            L.orc_nnz_footprint.argtypes = [_pp, C.c_int64]
+            L.orc_nnz_footprint.restype = C.c_int64
+            L.orc_hologram_window.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                              C.c_int64, _dp, _dp]
+            L.orc_hologram_window.restype = C.c_int64
             L.orc_n_tables.argtypes = [_pp]
             L.orc_n_tables.restype = C.c_int64
             L.orc_select.restype = C.c_int64
@@ -170,6 +179,31 @@ def haar_fwd(f: np.ndarray, L: int) -> np.ndarray:
     h, w = f.shape
     lib().orc_haar_fwd(_ptr(b, _dp), h, w, w, L)
     return b[..., 0] + 1j * b[..., 1]
+
+
+def filter_bank(wavelet: int):
+    """(h0, h1, off) of the wavelet's analysis filters (R-A21: coif1 closed form; Haar)."""
+    h0 = np.zeros(6); h1 = np.zeros(6); off = C.c_int()
+    taps = lib().orc_filter_bank(wavelet, _ptr(h0, _dp), _ptr(h1, _dp), C.byref(off))
+    return h0[:taps], h1[:taps], off.value
+
+
+def fb_fwd(wavelet: int, f: np.ndarray, L: int) -> np.ndarray:
+    b = _cplx_buf(f)
+    h, w = f.shape
+    lib().orc_fb_fwd(wavelet, _ptr(b, _dp), h, w, w, L)
+    return b[..., 0] + 1j * b[..., 1]
+
+
+def fb_inv(wavelet: int, f: np.ndarray, L: int) -> np.ndarray:
+    b = _cplx_buf(f)
+    h, w = f.shape
+    lib().orc_fb_inv(wavelet, _ptr(b, _dp), h, w, w, L)
+    return b[..., 0] + 1j * b[..., 1]
+
+
+def nnz_footprint(P: Params, t: int) -> int:
+    return int(lib().orc_nnz_footprint(C.byref(P.c()), int(t)))
 
 
 def haar_inv(f: np.ndarray, L: int) -> np.ndarray:
@@ -280,9 +314,13 @@ class Lut:
         return psi[..., 0] + 1j * psi[..., 1], cnt
 
     def hologram_window(self, pts, x0: int, y0: int, w: int, h: int):
-        """u = inverse FWT of psi on a 2^L-aligned window (steps 2-3)."""
-        psi, cnt = self.wasabi_window(pts, x0, y0, w, h)
-        return haar_inv(psi, self.P.levels), psi, cnt
+        """u = inverse FWT of psi on a 2^L-aligned window (steps 2-3; orc_hologram_window)."""
+        p = _pts64(pts)
+        u = np.zeros((h, w, 2))
+        psi = np.zeros((h, w, 2))
+        cnt = lib().orc_hologram_window(self.h, _ptr(p, _dp), p.shape[0], x0, y0, w, h, _ptr(u, _dp),
+                                        _ptr(psi, _dp))
+        return u[..., 0] + 1j * u[..., 1], psi[..., 0] + 1j * psi[..., 1], cnt
 
     def close(self):
         if self.h:

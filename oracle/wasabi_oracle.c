@@ -44,7 +44,7 @@ typedef struct {
     double z_min, z_max; /* depth range [m] */
     double retention;    /* r in (0,1] (north_star "top-r%") */
     int32_t exact;       /* 1: exact off-grid shifts via offset-class tables */
-    int32_t pad;
+    int32_t wavelet;     /* 0: Haar (R-A1); 1: coif1, the paper's coiflets (NEXT-2, R-A21) */
 } orc_params;
 
 /* R-A20 (NEXT-4): with exact = 1 every depth has 4^L tables, one per sub-position class
@@ -80,10 +80,13 @@ static double orc_radius_px(const orc_params *P, double z) {
     return fabs(z) * orc_tan_theta(P) / P->pitch;
 }
 
-/* Table half side H_d = 2^L (floor(R/2^L) + 1): table side 2H holds the disc and is 2^L aligned. */
+/* Table half side H_d = 2^L (floor(R/2^L) + 1): table side 2H holds the disc and is 2^L aligned.
+ * Coiflets (R-A21): the coefficients of a disc spread up to 3 (2^L - 1) px beyond it, so the table
+ * is padded: H = 2^L (floor((R + 3 2^L)/2^L) + 1) holds every nonzero coefficient exactly. */
 static int64_t orc_half(const orc_params *P, double R) {
     int64_t B = (int64_t)1 << P->levels;
-    return B * ((int64_t)floor(R / (double)B) + 1);
+    double pad = P->wavelet == 1 ? 3.0 * (double)B : 0.0;
+    return B * ((int64_t)floor((R + pad) / (double)B) + 1);
 }
 
 /* S_d membership: circ(c) = 1 iff c < 1, centre always kept (R-A17). */
@@ -95,7 +98,9 @@ static int orc_in_support(int64_t dx, int64_t dy, double R) {
 /* Structural nnz_d (R-A4): number of coefficient positions whose support block touches S_d.
  * Brute force over the mask: level-l detail coefficients (3 per 2^l block) and level-L
  * scaling coefficients (1 per 2^L block). */
+static int64_t orc_nnz_fb(const orc_params *P, int64_t side, int64_t Cx, int64_t Cy, double R);
 static int64_t orc_nnz_c(const orc_params *P, int64_t side, int64_t Cx, int64_t Cy, double R) {
+    if (P->wavelet == 1) return orc_nnz_fb(P, side, Cx, Cy, R);
     int64_t nnz = 0;
     unsigned char *m = (unsigned char *)calloc((size_t)(side * side), 1);
     for (int64_t Y = 0; Y < side; Y++)
@@ -115,6 +120,12 @@ static int64_t orc_nnz_c(const orc_params *P, int64_t side, int64_t Cx, int64_t 
     return nnz;
 }
 static int64_t orc_nnz(const orc_params *P, int64_t H, double R) { return orc_nnz_c(P, 2 * H, H, H, R); }
+
+/* Footprint E (reading R-A19's structural bound): a kept coefficient of a point lies within E px
+ * per axis: ceil(R) + 3 2^(L-1) for Haar; coiflet tables spread 3 2^L further (R-A21). */
+static int64_t orc_footprint(const orc_params *P, double R) {
+    return (int64_t)ceil(R) + (P->wavelet == 1 ? 7 : 3) * ((int64_t)1 << (P->levels - 1));
+}
 
 /* Table t geometry (R-A20): depth, H, side, PSF centre (Cx, Cy). */
 static void orc_table_geom(const orc_params *P, int64_t t, int *d, double *R, int64_t *H, int64_t *side,
@@ -154,7 +165,7 @@ int orc_geometry(const orc_params *P, double *z, double *R, int64_t *H, int64_t 
         if (z) z[d] = zd;
         if (R) R[d] = Rd;
         if (H) H[d] = Hd;
-        if (E) E[d] = (int64_t)ceil(Rd) + 3 * ((int64_t)1 << (P->levels - 1));
+        if (E) E[d] = orc_footprint(P, Rd);
         if (nnz || n_r) {
             int64_t c = orc_nnz(P, Hd, Rd);
             if (nnz) nnz[d] = c;
@@ -169,7 +180,7 @@ int orc_depth_info(const orc_params *P, int d, double *zr, int64_t *hen) {
     double zd = orc_level_z(P, d), Rd = orc_radius_px(P, zd);
     int64_t Hd = orc_half(P, Rd), c = orc_nnz(P, Hd, Rd);
     zr[0] = zd; zr[1] = Rd;
-    hen[0] = Hd; hen[1] = (int64_t)ceil(Rd) + 3 * ((int64_t)1 << (P->levels - 1));
+    hen[0] = Hd; hen[1] = orc_footprint(P, Rd);
     hen[2] = c; hen[3] = orc_n_r(P, c);
     return 0;
 }
@@ -195,6 +206,103 @@ int orc_psf_table(const orc_params *P, int64_t t, double *f) {
             o[1] = sin(ph);
         }
     return 0;
+}
+
+/* ---------------------------------------------------------------- filter banks (R-A21) */
+
+/* R-A21: "we used coiflets as the wavelets at level 3".
+ * The order is not given; coif1 (the shortest coiflet, 6 taps) in closed form (Daubechies'
+ * K = 1 coiflet):  h0 = sqrt(2)/32 [1-s, 5+s, 14+2s, 14-2s, 1-s, -3+s], s = sqrt(7), with
+ * h1[k] = (-1)^k h0[5-k].  Convention on the infinite grid (zero extension):
+ *   analysis  a[m] = sum_k h0[k] x[2m + k - off],  d[m] = sum_k h1[k] x[2m + k - off]
+ *   synthesis x[n] = sum_m h0[n - 2m + off] a[m] + h1[n - 2m + off] d[m]
+ * with off = 2 for coif1 (the filter's first moment about k = 2 vanishes, so a[m] samples
+ * x near 2m) and off = 0 for Haar (h0 = [1, 1]/sqrt2, h1 = [1, -1]/sqrt2), which reproduces the
+ * R-A6 butterflies.  Interleaved layout (R-A6): a level-l step works on the samples at multiples of
+ * 2^(l-1); a[m] goes to sample 2m (position 2^l m), d[m] to sample 2m + 1. */
+typedef struct { int taps, off; double h0[6], h1[6]; } orc_fb;
+
+static void orc_filters(int wavelet, orc_fb *F) {
+    memset(F, 0, sizeof *F);
+    if (wavelet == 1) {
+        double s7 = sqrt(7.0), c = sqrt(2.0) / 32.0;
+        double v[6] = {1.0 - s7, 5.0 + s7, 14.0 + 2.0 * s7, 14.0 - 2.0 * s7, 1.0 - s7, -3.0 + s7};
+        F->taps = 6; F->off = 2;
+        for (int k = 0; k < 6; k++) F->h0[k] = v[k] * c;
+    } else {
+        F->taps = 2; F->off = 0;
+        F->h0[0] = F->h0[1] = 1.0 / sqrt(2.0);
+    }
+    for (int k = 0; k < F->taps; k++) F->h1[k] = ((k & 1) ? -1.0 : 1.0) * F->h0[F->taps - 1 - k];
+}
+
+/* Filters of a wavelet (for the filter pins): h0, h1 (6 each, zero padded), returns taps; off out. */
+int orc_filter_bank(int wavelet, double *h0, double *h1, int *off) {
+    orc_fb F;
+    orc_filters(wavelet, &F);
+    for (int k = 0; k < 6; k++) { h0[k] = F.h0[k]; h1[k] = F.h1[k]; }
+    *off = F.off;
+    return F.taps;
+}
+
+/* One analysis (dir = +1) or synthesis (dir = -1) step along a line of N complex samples, sample n at
+ * f + 2 n st; N even.  Zero extension beyond [0, N).  Sums in tap order k = 0..taps-1. */
+static void orc_fb_line(const orc_fb *F, double *f, int64_t st, int64_t N, int dir, double *tmp) {
+    for (int64_t n = 0; n < N; n++) { tmp[2 * n] = f[2 * n * st]; tmp[2 * n + 1] = f[2 * n * st + 1]; }
+    if (dir > 0) {
+        for (int64_t m = 0; m < N / 2; m++)
+            for (int c = 0; c < 2; c++) {
+                double a = 0.0, d = 0.0;
+                for (int k = 0; k < F->taps; k++) {
+                    int64_t i = 2 * m + k - F->off;
+                    if (i < 0 || i >= N) continue;
+                    a += F->h0[k] * tmp[2 * i + c];
+                    d += F->h1[k] * tmp[2 * i + c];
+                }
+                f[2 * (2 * m) * st + c] = a;
+                f[2 * (2 * m + 1) * st + c] = d;
+            }
+    } else {
+        for (int64_t n = 0; n < N; n++)
+            for (int c = 0; c < 2; c++) {
+                double x = 0.0;
+                /* k = n - 2m + off in [0, taps): m from (n + off)/2 down to (n + off - taps + 1)/2 */
+                int64_t m_hi = (n + F->off) / 2, m_lo = m_hi - F->taps / 2 - 1;
+                for (int64_t m = m_lo; m <= m_hi; m++) {
+                    int64_t k = n - 2 * m + F->off;
+                    if (m < 0 || m >= N / 2 || k < 0 || k >= F->taps) continue;
+                    x += F->h0[k] * tmp[2 * (2 * m) + c];
+                    x += F->h1[k] * tmp[2 * (2 * m + 1) + c];
+                }
+                f[2 * n * st + c] = x;
+            }
+    }
+}
+
+/* L-level 2-D forward (rows, then columns, per level) / inverse (columns, then rows, levels L..1)
+ * of a rows x cols interleaved complex array (row stride `stride`), zero extension. */
+void orc_fb_fwd(int wavelet, double *f, int64_t rows, int64_t cols, int64_t stride, int L) {
+    orc_fb F;
+    orc_filters(wavelet, &F);
+    double *tmp = (double *)malloc(sizeof(double) * 2 * (size_t)(rows > cols ? rows : cols));
+    for (int l = 1; l <= L; l++) {
+        int64_t s = (int64_t)1 << (l - 1);
+        for (int64_t Y = 0; Y < rows; Y += s) orc_fb_line(&F, f + 2 * (Y * stride), s, cols / s, +1, tmp);
+        for (int64_t X = 0; X < cols; X += s) orc_fb_line(&F, f + 2 * X, s * stride, rows / s, +1, tmp);
+    }
+    free(tmp);
+}
+
+void orc_fb_inv(int wavelet, double *f, int64_t rows, int64_t cols, int64_t stride, int L) {
+    orc_fb F;
+    orc_filters(wavelet, &F);
+    double *tmp = (double *)malloc(sizeof(double) * 2 * (size_t)(rows > cols ? rows : cols));
+    for (int l = L; l >= 1; l--) {
+        int64_t s = (int64_t)1 << (l - 1);
+        for (int64_t X = 0; X < cols; X += s) orc_fb_line(&F, f + 2 * X, s * stride, rows / s, -1, tmp);
+        for (int64_t Y = 0; Y < rows; Y += s) orc_fb_line(&F, f + 2 * (Y * stride), s, cols / s, -1, tmp);
+    }
+    free(tmp);
 }
 
 /* ---------------------------------------------------------------- Haar (steps 1, 3) */
@@ -277,8 +385,37 @@ int orc_table_coeffs(const orc_params *P, int64_t t, double *coef) {
     int d; double R; int64_t H, side, Cx, Cy;
     orc_table_geom(P, t, &d, &R, &H, &side, &Cx, &Cy);
     orc_psf_table(P, t, coef);
-    orc_haar_fwd(coef, side, side, side, P->levels);
+    if (P->wavelet == 1) orc_fb_fwd(1, coef, side, side, side, P->levels);   /* coif1, R-A21 */
+    else orc_haar_fwd(coef, side, side, side, P->levels);
     return 0;
+}
+
+/* Structural nnz of a filter-bank transform (R-A21; with Haar filters it equals the block count):
+ * the coefficient of level l at index (m, n) = (X >> l, Y >> l) depends on the input rectangle
+ * [2^l m - off (2^l - 1), 2^l m + (taps - 1 - off)(2^l - 1)] (same in Y); it can be nonzero iff the
+ * rectangle meets S_d, i.e. iff the rectangle's lattice point nearest to the centre is in S_d. */
+static int64_t orc_nnz_fb(const orc_params *P, int64_t side, int64_t Cx, int64_t Cy, double R) {
+    orc_fb F;
+    orc_filters(P->wavelet, &F);
+    int64_t nnz = 0;
+    for (int64_t Y = 0; Y < side; Y++)
+        for (int64_t X = 0; X < side; X++) {
+            int lv, bd;
+            orc_classify(X, Y, P->levels, &lv, &bd);
+            int64_t b = (int64_t)1 << lv, mx = X >> lv, my = Y >> lv;
+            int64_t x0 = b * mx - F.off * (b - 1), x1 = b * mx + (F.taps - 1 - F.off) * (b - 1);
+            int64_t y0 = b * my - F.off * (b - 1), y1 = b * my + (F.taps - 1 - F.off) * (b - 1);
+            int64_t nx = Cx < x0 ? x0 : (Cx > x1 ? x1 : Cx), ny = Cy < y0 ? y0 : (Cy > y1 ? y1 : Cy);
+            if (orc_in_support(nx - Cx, ny - Cy, R)) nnz++;
+        }
+    return nnz;
+}
+
+/* Structural nnz by the filter-bank footprint rule for any wavelet (pin: Haar == block count). */
+int64_t orc_nnz_footprint(const orc_params *P, int64_t t) {
+    int d; double R; int64_t H, side, Cx, Cy;
+    orc_table_geom(P, t, &d, &R, &H, &side, &Cx, &Cy);
+    return orc_nnz_fb(P, side, Cx, Cy, R);
 }
 
 /* PAPER.md:92 "select N_r strong coefficients among the wavelet-domain PSF and store them in
@@ -537,13 +674,13 @@ int64_t orc_wasabi_window(void *lut, const double *pts, int64_t n, int64_t x0, i
     orc_lut *t = (orc_lut *)lut;
     const orc_params *P = &t->P;
     memset(psi, 0, sizeof(double) * 2 * (size_t)(w * h));
-    int64_t count = 0, half = (int64_t)1 << (P->levels - 1);
+    int64_t count = 0;
     for (int64_t j = 0; j < n; j++) {
         int64_t ix, iy;
         int iz;
         if (!orc_point(P, pts + 4 * j, &ix, &iy, &iz)) continue;
         double R = orc_radius_px(P, orc_level_z(P, iz));
-        int64_t E = (int64_t)ceil(R) + 3 * half;
+        int64_t E = orc_footprint(P, R);
         if (ix + E < x0 || ix - E >= x0 + w || iy + E < y0 || iy - E >= y0 + h) continue;
         orc_depth_list *L = orc_lut_get(t, orc_point_table(P, ix, iy, iz));
         double a = pts[4 * j + 3];
@@ -560,6 +697,31 @@ int64_t orc_wasabi_window(void *lut, const double *pts, int64_t n, int64_t x0, i
         }
     }
     return count;
+}
+
+/* Steps 2b + 3 on a window (x0, y0, w, h multiples of 2^L): psi by Eq.(2) (orc_wasabi_window) and
+ * u = inverse FWT.  Haar: blocks are 2^L-local, so the window's own psi suffices.
+ * Coiflets (R-A21): u at the window needs psi up to 3 (2^L - 1) px beyond it, so psi is formed on
+ * the window grown by 64 px per side (clipped to the hologram: coefficients outside [0, N_h)^2 are
+ * dropped, R-A12) and inverted with zero extension; u and psi are returned on the window. */
+int64_t orc_hologram_window(void *lut, const double *pts, int64_t n, int64_t x0, int64_t y0, int64_t w,
+                            int64_t h, double *u, double *psi) {
+    orc_lut *t = (orc_lut *)lut;
+    const orc_params *P = &t->P;
+    int64_t g = P->wavelet == 1 ? 64 : 0;
+    int64_t ex0 = x0 - g < 0 ? 0 : x0 - g, ey0 = y0 - g < 0 ? 0 : y0 - g;
+    int64_t ex1 = x0 + w + g > P->n_h ? P->n_h : x0 + w + g, ey1 = y0 + h + g > P->n_h ? P->n_h : y0 + h + g;
+    int64_t ew = ex1 - ex0, eh = ey1 - ey0;
+    double *pe = (double *)malloc(sizeof(double) * 2 * (size_t)(ew * eh));
+    int64_t cnt = orc_wasabi_window(lut, pts, n, ex0, ey0, ew, eh, pe);
+    for (int64_t Y = 0; Y < h; Y++)
+        memcpy(psi + 2 * (Y * w), pe + 2 * ((Y + y0 - ey0) * ew + (x0 - ex0)), sizeof(double) * 2 * (size_t)w);
+    if (P->wavelet == 1) orc_fb_inv(1, pe, eh, ew, ew, P->levels);
+    else orc_haar_inv(pe, eh, ew, ew, P->levels);
+    for (int64_t Y = 0; Y < h; Y++)
+        memcpy(u + 2 * (Y * w), pe + 2 * ((Y + y0 - ey0) * ew + (x0 - ex0)), sizeof(double) * 2 * (size_t)w);
+    free(pe);
+    return cnt;
 }
 
 /* ---------------------------------------------------------------- quantise (step 4) */

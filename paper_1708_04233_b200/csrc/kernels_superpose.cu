@@ -14,10 +14,9 @@
 // (float2 value + uint16 position) and does one read-modify-write in shared memory.  A chunk never
 // mixes points, so its targets are distinct; chunks run in point order for each level, so every
 // pixel (which belongs to exactly one level) accumulates in point order: bitwise deterministic
-// and independent of the band split (R-A11).  Chunks are issued in groups of up to kD chunks of one
-// range, double-buffered: the (predicated, never-waited) loads of the next group are in flight
-// while the current group is consumed, and one bulk L2 prefetch per range and array is issued when
-// a batch's ranges are known.  Column overrun of the level-1/2 column groups lands in kWinMargin
+// and independent of the band split (R-A11).  A kD-deep register ring keeps the loads of the next
+// chunks in flight across range, level and batch boundaries (idle lanes address the warp's dummy
+// cell).  Column overrun of the level-1/2 column groups lands in kWinMargin
 // margin columns of the shared tile (never read).  The kernel is bound by the L1TEX/LSU data pipe
 // (scattered 8-byte shared-memory read-modify-writes with random bank conflicts + the LUT loads;
 // DESIGN.md §6).
@@ -42,23 +41,10 @@ struct SupArgs {
 #define WASABI_MINB 6
 #endif
 #ifndef WASABI_PF
-#define WASABI_PF 1
+#define WASABI_PF 0   // bulk L2 prefetch of each batch's ranges: measured slower with the ring at full C4
 #endif
-#ifndef WASABI_PRED_IDLE
-#define WASABI_PRED_IDLE 0
-#endif
-constexpr int kD = WASABI_KD;          // chunks per group (two groups in flight per warp)
 
-// Predicated read-only loads: the destination keeps its previous value when c is false, and the
-// load never forces a wait on its result (the selects happen in the consumer).
-__device__ __forceinline__ void ldg_v2_if(float2 &v, const float2 *p, bool c) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.nc.v2.f32 {%0, %1}, [%2];\n\t}"
-                 : "+f"(v.x), "+f"(v.y) : "l"(p), "r"((int)c));
-}
-__device__ __forceinline__ void ldg_u16_if(int &v, const uint16_t *p, bool c) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u16 %0, [%1];\n\t}"
-                 : "+r"(v) : "l"(p), "r"((int)c));
-}
+constexpr int kD = WASABI_KD;          // register ring depth (chunks in flight per warp)
 
 // Bulk prefetch of [p, p + bytes) into L2 (16-byte granules): one instruction per range, so the
 // later chunks of a range hit L2 instead of waiting on DRAM.
@@ -231,58 +217,51 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         next_range();
     }
 
-    // Groups of up to kG chunks of one range, double-buffered (A, B): the loads of the next group
-    // are issued before the current group is consumed.  Idle lanes carry a position that points
-    // at the warp's dummy cell (their stale value only ever reaches it).
-    constexpr int kG = kD;
-    float2 va[kG], vb[kG];
-    int pa[kG], pb_[kG];
-    uint32_t saA = 0u, saB = 0u;
-    float aA = 0.f, aB = 0.f;
-    int nA = 0, nB = 0, dA = 0, dB = 0;
+    // kD-deep register ring of chunks, continuous across range, level and batch boundaries
+    // (slot: value, position, smem byte base of the range or of the dummy cell, a_j)
+    const uint32_t dummy_sa = tile_sa + 8u * (uint32_t)dummy;
+    float2 rv[kD];
+    int rp[kD];
+    uint32_t rb[kD];
+    float ra[kD];
 #pragma unroll
-    for (int u = 0; u < kG; u++) { va[u] = make_float2(0.f, 0.f); vb[u] = va[u]; pa[u] = 0; pb_[u] = 0; }
-#define WASABI_FILL(V, P, SA, AA, N, DP)                                            \
+    for (int u = 0; u < kD; u++) rv[u] = make_float2(0.f, 0.f);
+#define WASABI_PREFETCH(u)                                                          \
     do {                                                                            \
-        N = 0;                                                                      \
+        const int e = c_beg + lane;                                                 \
+        const bool v = have && e < c_end;                                           \
+        rp[u] = 0;                                                                  \
+        if (v) {                                                                    \
+            rv[u] = __ldg(vval + e);                                                \
+            rp[u] = __ldg(vpos + e);                                                \
+        }                                                                           \
+        rb[u] = v ? c_sa : dummy_sa;                                                \
+        ra[u] = c_a;                                                                \
         if (have) {                                                                 \
-            SA = c_sa; AA = c_a; DP = c_dpos;                                       \
-            N = min(kG, (c_end - c_beg + 31) >> 5);                                 \
-            const int e0 = c_beg + lane, last = c_end - 1 - e0;                     \
-            const float2 *vp = vval + e0;                                           \
-            const uint16_t *pp = vpos + e0;                                         \
-            _Pragma("unroll") for (int u = 0; u < kG; u++) {                        \
-                /* values: whole chunks (the LUT is padded); positions: idle lanes keep \
-                   the dummy position */                                            \
-                ldg_v2_if(V[u], vp + 32 * u, u < N);                                \
-                P[u] = c_dpos;                                                      \
-                ldg_u16_if(P[u], pp + 32 * u, u < N && 32 * u <= last);            \
-            }                                                                       \
-            c_beg += 32 * N;                                                        \
+            c_beg += 32;                                                            \
             if (c_beg >= c_end) next_range();                                       \
         }                                                                           \
     } while (0)
-#define WASABI_CONSUME(V, P, SA, AA, N, DP)                                         \
+#define WASABI_CONSUME(u)                                                           \
     do {                                                                            \
-        _Pragma("unroll") for (int u = 0; u < kG; u++) {                            \
-            if (u < N && (!WASABI_PRED_IDLE || P[u] != DP)) {                       \
-                const uint32_t sa = SA + 8u * (uint32_t)P[u];                       \
-                float2 o = lds2(sa);                                                \
-                o.x = fmaf(AA, V[u].x, o.x);                                        \
-                o.y = fmaf(AA, V[u].y, o.y);                                        \
-                sts2(sa, o);                                                        \
-            }                                                                       \
-        }                                                                           \
+        const uint32_t sa = rb[u] + 8u * (uint32_t)rp[u];                           \
+        float2 o = lds2(sa);                                                        \
+        o.x = fmaf(ra[u], rv[u].x, o.x);                                            \
+        o.y = fmaf(ra[u], rv[u].y, o.y);                                            \
+        sts2(sa, o);                                                                \
     } while (0)
-    WASABI_FILL(va, pa, saA, aA, nA, dA);
-    while (nA > 0) {
-        WASABI_FILL(vb, pb_, saB, aB, nB, dB);
-        WASABI_CONSUME(va, pa, saA, aA, nA, dA);
-        if (nB == 0) break;
-        WASABI_FILL(va, pa, saA, aA, nA, dA);
-        WASABI_CONSUME(vb, pb_, saB, aB, nB, dB);
+#pragma unroll
+    for (int u = 0; u < kD; u++) WASABI_PREFETCH(u);
+    bool more = true;
+    while (more) {
+        more = have;
+#pragma unroll
+        for (int u = 0; u < kD; u++) {
+            WASABI_CONSUME(u);
+            WASABI_PREFETCH(u);
+        }
     }
-#undef WASABI_FILL
+#undef WASABI_PREFETCH
 #undef WASABI_CONSUME
     __syncthreads();
     float2 *data = tile + M;                    // row r, column x at data[r * S + x]
