@@ -80,6 +80,19 @@ typedef struct {
  * (0 <= t < wasabi_table_count). */
 #define WASABI_FLAG_EXACT_SHIFT 1u
 
+/* Coiflets, the paper's wavelet ("coiflets as the wavelets at level 3"; SURVEY.md
+ * §8(f) NEXT-2, reading R-A21; needs levels <= 4, n_h <= 16384, not with EXACT_SHIFT).  The tables
+ * use the coif1 filter bank (6 taps) on the interleaved layout with zero extension, padded so every
+ * nonzero coefficient is kept in the table; the superposition is unchanged.  The inverse is not
+ * block-local: u on rows [row0, row1) needs psi on the HALO band [max(0, row0 - H), min(n_h, row1 +
+ * H)), H = wasabi_coif_halo_rows(params), so: wasabi_bin_points + wasabi_superpose on the halo band,
+ * then wasabi_inverse_wt (d_psi = that halo band, transformed in place).  wasabi_superpose_inverse
+ * (the fused Haar kernel) returns EINVAL in this mode; wasabi_hologram_host handles it. */
+#define WASABI_FLAG_COIFLET 2u
+
+/* Rows of psi halo the coiflet inverse needs on each side of a band (= tile; 0 for Haar). */
+int64_t wasabi_coif_halo_rows(const wasabi_params *params);
+
 /* Spherical reference wave point (paper default (0, 0.030, -0.400) m). */
 typedef struct {
     double x_r_m, y_r_m, z_r_m;
@@ -156,7 +169,11 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
 
 /* Step 3: L-level inverse Haar, tile-local (band rows multiples of 2^L, so
  * no halo).  d_u may alias d_psi (in place).  d_u == NULL: u is not written (print only).
- * d_bits != NULL fuses step 4 (see wasabi_quantize) and requires `print`. */
+ * d_bits != NULL fuses step 4 (see wasabi_quantize) and requires `print`.
+ * WASABI_FLAG_COIFLET: d_psi is the halo band [max(0, row0 - H), min(n_h, row1 + H)) x n_h
+ * (H = wasabi_coif_halo_rows), synthesised IN PLACE (coif1, zero outside the band and the
+ * hologram); rows [row0, row1) of the result are u.  d_u (rows [row0, row1)) may be NULL, may be
+ * the matching row of d_psi (no copy), or another buffer (copied). */
 wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi, float *d_u, int64_t row0,
                                 int64_t row1, const wasabi_print_params *print, uint8_t *d_bits,
                                 cudaStream_t stream);

@@ -18,6 +18,7 @@ WASABI_OK, WASABI_EINVAL, WASABI_ENOSPC, WASABI_ECUDA, WASABI_ESTATE = 0, -1, -2
 
 
 FLAG_EXACT_SHIFT = 1   # include/wasabi.h WASABI_FLAG_EXACT_SHIFT
+FLAG_COIFLET = 2       # include/wasabi.h WASABI_FLAG_COIFLET
 
 
 class WasabiError(RuntimeError):
@@ -55,6 +56,7 @@ class Params:
     retention: float
     tile: int = 64
     exact: bool = False   # WASABI_FLAG_EXACT_SHIFT: offset-class tables (R-A20)
+    wavelet: int = 0      # 0 Haar; 1 WASABI_FLAG_COIFLET: coif1, the paper's coiflets (R-A21, NEXT-2)
 
     @staticmethod
     def from_config(cfg, **kw) -> "Params":
@@ -64,7 +66,12 @@ class Params:
 
     def c(self) -> _CParams:
         return _CParams(self.wavelength, self.pitch, self.n_h, self.n_depth, self.levels, self.z_min,
-                        self.z_max, self.retention, self.tile, FLAG_EXACT_SHIFT if self.exact else 0)
+                        self.z_max, self.retention, self.tile,
+                        (FLAG_EXACT_SHIFT if self.exact else 0) | (FLAG_COIFLET if self.wavelet == 1 else 0))
+
+    def halo_rows(self) -> int:
+        """psi rows the inverse needs beyond a band on each side (wasabi_coif_halo_rows)."""
+        return int(lib().wasabi_coif_halo_rows(C.byref(self.c())))
 
 
 @dataclasses.dataclass(frozen=True)
@@ -97,6 +104,8 @@ def lib() -> C.CDLL:
         L.wasabi_version.restype = C.c_char_p
         L.wasabi_kernel_launches.restype = C.c_ulonglong
         L.wasabi_kernel_launches.argtypes = []
+        L.wasabi_coif_halo_rows.restype = C.c_int64
+        L.wasabi_coif_halo_rows.argtypes = [_PP]
         sig = {
             "wasabi_psf_tables_bytes": [_PP, C.POINTER(_sz), C.POINTER(_sz)],
             "wasabi_build_psf_tables": [_PP, _vp, _sz, _vp, _sz, _vp],

@@ -13,9 +13,10 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
                  "-I", CSRC, "-Xptxas", "-warn-spills"] + os.environ.get("WASABI_NVCC_DEFS", "").split()
 # the table kernels compute the fp32 rank keys with the specification's exact IEEE sequence
-PER_FILE = {"kernels_tables.cu": ["--fmad=false"], "kernels_direct.cu": ["--fmad=false"]}
+PER_FILE = {"kernels_tables.cu": ["--fmad=false"], "kernels_direct.cu": ["--fmad=false"],
+            "kernels_coif.cu": ["--fmad=false"]}
 SOURCES = ["kernels_tables.cu", "kernels_scan.cu", "kernels_bins.cu", "kernels_superpose.cu",
-           "kernels_inverse.cu", "kernels_direct.cu", "wasabi_host.cpp"]
+           "kernels_inverse.cu", "kernels_direct.cu", "kernels_coif.cu", "wasabi_host.cpp"]
 
 
 def _stale(obj, src):

@@ -94,7 +94,8 @@ struct TableHeader {
     int64_t vent_cap;                  // window-LUT entry capacity (bound: 16 N_r per depth)
     int64_t vptr_off, vval_off, vpos_off;  // window LUT: pointers, float2 values, uint16 positions
     int32_t cls_bits, n_zlevels;       // offset-class bits cb (0 or L) and depth levels N_z
-    int64_t pad[2];
+    int32_t wavelet, pad1;             // 0 Haar, 1 coif1 (R-A21)
+    int64_t pad[1];
 };
 static_assert(sizeof(TableHeader) <= 256, "table header must fit the 256-byte slot");
 
@@ -141,6 +142,13 @@ cudaError_t launch_select(const TableHeader &h, const void *d_tables, const uint
 cudaError_t launch_groups(const TableHeader &h, void *d_tables, const float2 *coef_val, const uint32_t *coef_key,
                           const unsigned long long *sel_state, int pass, cudaStream_t s);
 cudaError_t launch_vgroups(const TableHeader &h, void *d_tables, int pass, cudaStream_t s);
+// coiflet mode (R-A21): fp64 PSF + L-level coif1 analysis of every table (work/tmp: fp64 tables,
+// d_pre: per level the (n_tables + 1) prefix of (lines x pairs) work items, h_pre_last: its totals)
+cudaError_t launch_coif_tables(const TableHeader &h, const void *d_tables, double2 *work, double2 *tmp,
+                               const int64_t *d_pre, const int64_t *h_pre_last, float2 *val, uint32_t *key,
+                               int64_t n_coef, double k, double pitch, int L, cudaStream_t s);
+// coif1 synthesis of a psi band (nrows x n_h) in place, levels L..1
+cudaError_t launch_coif_inverse(float2 *psi, int64_t nrows, int64_t n_h, int L, cudaStream_t s);
 cudaError_t launch_scan_i32(int32_t *data, int64_t n, void *scratch, cudaStream_t s);
 cudaError_t launch_scan_u32_to_u64(const uint32_t *in, unsigned long long *out, int64_t n, void *scratch,
                                    cudaStream_t s);

@@ -82,9 +82,16 @@ wasabi_status validate(const wasabi_params *P) {
     if (P->n_depth > 1 && !(P->z_max_m > P->z_min_m)) return fail(WASABI_EINVAL, "n_depth > 1 needs z_max > z_min");
     if (!(P->retention > 0) || P->retention > 1) return fail(WASABI_EINVAL, "retention must be in (0, 1]");
     if (llround(P->retention * 1e6) < 1) return fail(WASABI_EINVAL, "retention below 1 ppm");
-    if (P->flags & ~(uint32_t)WASABI_FLAG_EXACT_SHIFT) return fail(WASABI_EINVAL, "unknown flags 0x%x", P->flags);
+    if (P->flags & ~(uint32_t)(WASABI_FLAG_EXACT_SHIFT | WASABI_FLAG_COIFLET))
+        return fail(WASABI_EINVAL, "unknown flags 0x%x", P->flags);
     if ((P->flags & WASABI_FLAG_EXACT_SHIFT) && P->levels > 4)
         return fail(WASABI_EINVAL, "WASABI_FLAG_EXACT_SHIFT needs levels <= 4 (4^L offset-class tables per depth)");
+    if (P->flags & WASABI_FLAG_COIFLET) {
+        if (P->flags & WASABI_FLAG_EXACT_SHIFT)
+            return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET cannot be combined with WASABI_FLAG_EXACT_SHIFT");
+        if (P->levels > 4) return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET needs levels <= 4 (psi halo of one tile)");
+        if (P->n_h > 16384) return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET needs n_h <= 16384 (line synthesis in shared memory)");
+    }
     return WASABI_OK;
 }
 
@@ -128,10 +135,33 @@ int64_t nnz_structural(int64_t side, int64_t Cx, int64_t Cy, double R, int L) {
     return nnz;
 }
 
+// Structural nnz of the coif1 transform (R-A21): the coefficient of level l at index (m, n) =
+// (X >> l, Y >> l) depends on the input rectangle [2^l m - 2 (2^l - 1), 2^l m + 3 (2^l - 1)] per axis
+// (6 taps, offset 2); it can be nonzero iff that rectangle meets S_d, i.e. iff its lattice point
+// nearest to the centre (C, C) is in S_d.  Level of a position: t = trailing zeros common to X and Y.
+int64_t nnz_coif(int64_t side, int64_t C, double R, int L) {
+    int64_t nnz = 0;
+    for (int64_t Y = 0; Y < side; Y++)
+        for (int64_t X = 0; X < side; X++) {
+            int t = 0;
+            while (t < L && !((X >> t) & 1) && !((Y >> t) & 1)) t++;
+            const int l = t >= L ? L : t + 1;
+            const int64_t b = 1ll << l, mx = X >> l, my = Y >> l;
+            const int64_t x0 = b * mx - 2 * (b - 1), x1 = b * mx + 3 * (b - 1);
+            const int64_t y0 = b * my - 2 * (b - 1), y1 = b * my + 3 * (b - 1);
+            const int64_t nx = std::min(std::max(C, x0), x1), ny = std::min(std::max(C, y0), y1);
+            if (in_support(nx - C, ny - C, R)) nnz++;
+        }
+    return nnz;
+}
+
 struct Geo {
     wasabi_params P;
     double k, tan_theta, dz;
     int T, S, L, nd, nz, cb;   // nd = tables, nz = depth levels, cb = offset-class bits (R-A20)
+    int wav = 0;               // 1: coif1 tables (R-A21)
+    std::vector<int64_t> pre;  // coif: per level, (nd + 1) prefix of analysis work items
+    size_t sc_work = 0, sc_tmp = 0, sc_pre = 0;
     std::vector<KDesc> kd;
     std::vector<DDesc> dd;
     std::vector<int32_t> ctabase;
@@ -153,6 +183,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     g.T = P->tile; g.S = P->tile + kWinMargin; g.L = P->levels; g.nz = P->n_depth;
     g.cb = (P->flags & WASABI_FLAG_EXACT_SHIFT) ? P->levels : 0;
     g.nd = P->n_depth << (2 * g.cb);
+    g.wav = (P->flags & WASABI_FLAG_COIFLET) ? 1 : 0;
     g.k = 2.0 * kPi / P->wavelength_m;
     const double sigma = P->wavelength_m / (2.0 * P->pitch_m);
     g.tan_theta = sigma / std::sqrt(1.0 - sigma * sigma);
@@ -167,12 +198,13 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
         const int cx = d & ((1 << g.cb) - 1), cy = (d >> g.cb) & ((1 << g.cb) - 1);
         const double z = level_z(*P, g.dz, zi);
         const double R = std::fabs(z) * g.tan_theta / P->pitch_m;
-        const int64_t H = B * ((int64_t)std::floor(R / (double)B) + 1);
+        // coif1 tables are padded by 3 2^L so every nonzero coefficient of the disc stays inside (R-A21)
+        const int64_t H = B * ((int64_t)std::floor((R + (g.wav ? 3.0 * (double)B : 0.0)) / (double)B) + 1);
         const int64_t side = 2 * H + (g.cb ? B : 0);
         if (side > kMaxTableSide)
             return fail(WASABI_EINVAL, "depth %d: PSF table side %lld exceeds %d (|z| too large for this pitch)", zi,
                         (long long)side, kMaxTableSide);
-        const int64_t E = (int64_t)std::ceil(R) + 3 * (1ll << (g.L - 1));
+        const int64_t E = (int64_t)std::ceil(R) + (g.wav ? 7 : 3) * (1ll << (g.L - 1));
         DDesc &D = g.dd[d];
         KDesc &K = g.kd[d];
         D.z = z; D.R = R;
@@ -204,7 +236,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
             vptr += win_slots(D.side, l, g.cb);
         }
         for (int l = g.L + 1; l <= kMaxLevels; l++) K.vptr_base[l - 1] = (int32_t)vptr;
-        D.nnz = nnz_structural(side, H + cx, H + cy, R, g.L);
+        D.nnz = g.wav ? nnz_coif(side, H, R, g.L) : nnz_structural(side, H + cx, H + cy, R, g.L);
         {
             const int64_t r_ppm = llround(P->retention * 1e6);
             const int64_t n = (r_ppm * D.nnz + 999999) / 1000000;
@@ -223,7 +255,7 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     h.magic = kTableMagic;
     h.param_hash = param_hash(*P);
     h.n_depth = g.nd; h.levels = g.L; h.tile = g.T; h.S = g.S;
-    h.cls_bits = g.cb; h.n_zlevels = g.nz;
+    h.cls_bits = g.cb; h.n_zlevels = g.nz; h.wavelet = g.wav;
     h.total_entries = entries; h.total_ptrs = ptr; h.total_ctas = ctas;
     size_t off = 256;
     h.kdesc_off = off; off = align_up(off + sizeof(KDesc) * g.nd, 256);
@@ -247,6 +279,17 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
     g.sc_hist = so; so = align_up(so + 4 * 256 * (size_t)g.nd, 256);
     g.sc_sel = so; so = align_up(so + 24 * (size_t)g.nd, 256);
     g.sc_scan = so; so = align_up(so + scan_scratch_bytes(std::max(ptr, vptr) + 1), 256);
+    if (g.wav) {   // fp64 work and ping-pong tables, per-level work-item prefixes
+        g.pre.assign((size_t)g.L * (g.nd + 1), 0);
+        for (int l = 1; l <= g.L; l++)
+            for (int d = 0; d < g.nd; d++) {
+                const int64_t N = (int64_t)g.dd[d].side >> (l - 1);
+                g.pre[(size_t)(l - 1) * (g.nd + 1) + d + 1] = g.pre[(size_t)(l - 1) * (g.nd + 1) + d] + N * (N / 2);
+            }
+        g.sc_work = so; so = align_up(so + 16 * (size_t)coef, 256);
+        g.sc_tmp = so; so = align_up(so + 16 * (size_t)coef, 256);
+        g.sc_pre = so; so = align_up(so + 8 * g.pre.size(), 256);
+    }
     g.scratch_bytes = so;
     return WASABI_OK;
 }
@@ -321,6 +364,11 @@ wasabi_status wasabi_depth_geometry(const wasabi_params *params, int32_t depth, 
     return WASABI_OK;
 }
 
+int64_t wasabi_coif_halo_rows(const wasabi_params *params) {
+    // the coif1 synthesis of L <= 4 levels reaches 3 (2^L - 1) <= 45 rows: one tile (a multiple of it)
+    return (params && (params->flags & WASABI_FLAG_COIFLET)) ? (int64_t)std::max(64, params->tile) : 0;
+}
+
 wasabi_status wasabi_table_count(const wasabi_params *params, int64_t *n_tables) {
     Geo g;
     wasabi_status st = compute_geo(params, g);
@@ -346,7 +394,17 @@ wasabi_status wasabi_build_psf_tables(const wasabi_params *params, void *d_table
     CK(launch_write_blob(tb + g.th.ctabase_off, g.ctabase.data(), 4 * (g.nd + 1), stream), "write ctabase");
     float2 *cval = reinterpret_cast<float2 *>(sb + g.sc_val);
     uint32_t *ckey = reinterpret_cast<uint32_t *>(sb + g.sc_key);
-    CK(launch_psf_haar(g.th, d_tables, cval, ckey, g.k, params->pitch_m, g.L, g.nd, stream), "psf_haar");
+    if (g.wav) {
+        std::vector<int64_t> last(g.L);
+        for (int l = 1; l <= g.L; l++) last[l - 1] = g.pre[(size_t)(l - 1) * (g.nd + 1) + g.nd];
+        CK(launch_write_blob(sb + g.sc_pre, g.pre.data(), 8 * g.pre.size(), stream), "write coif prefixes");
+        CK(launch_coif_tables(g.th, d_tables, reinterpret_cast<double2 *>(sb + g.sc_work),
+                              reinterpret_cast<double2 *>(sb + g.sc_tmp), reinterpret_cast<const int64_t *>(sb + g.sc_pre),
+                              last.data(), cval, ckey, g.total_coef, g.k, params->pitch_m, g.L, stream),
+           "coif tables");
+    } else {
+        CK(launch_psf_haar(g.th, d_tables, cval, ckey, g.k, params->pitch_m, g.L, g.nd, stream), "psf_haar");
+    }
     CK(launch_select(g.th, d_tables, ckey, reinterpret_cast<unsigned int *>(sb + g.sc_hist),
                      reinterpret_cast<unsigned long long *>(sb + g.sc_sel), g.nd, stream),
        "select");
@@ -419,6 +477,9 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
     if (st != WASABI_OK) return st;
     if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
     if (!d_tables || !d_bins) return fail(WASABI_EINVAL, "NULL buffer");
+    if (params->flags & WASABI_FLAG_COIFLET)
+        return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET: the coiflet inverse is not tile-local; use wasabi_superpose "
+                                   "on the halo band + wasabi_inverse_wt");
     if (d_bits && !print) return fail(WASABI_EINVAL, "d_bits needs print params");
     if (!aligned(d_u, 16)) return fail(WASABI_EINVAL, "d_u must be 16-byte aligned");
     double p4[4];
@@ -443,6 +504,19 @@ wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi,
     if (!aligned(d_psi, 16) || !aligned(d_u, 16)) return fail(WASABI_EINVAL, "fields must be 16-byte aligned");
     double p4[4];
     if (print) { p4[0] = print->x_r_m; p4[1] = print->y_r_m; p4[2] = print->z_r_m; p4[3] = 1.0 / params->wavelength_m; }
+    if (params->flags & WASABI_FLAG_COIFLET) {   // R-A21: in place on the halo band, then u rows, then bits
+        const int64_t H = wasabi_coif_halo_rows(params);
+        const int64_t e0 = std::max<int64_t>(0, row0 - H), e1 = std::min<int64_t>(params->n_h, row1 + H);
+        float2 *pe = reinterpret_cast<float2 *>(const_cast<float *>(d_psi));
+        if (e1 > e0) CK(launch_coif_inverse(pe, e1 - e0, params->n_h, params->levels, stream), "coif inverse");
+        float2 *uc = pe + (row0 - e0) * params->n_h;
+        if (d_u && reinterpret_cast<float2 *>(d_u) != uc && row1 > row0)
+            CK(cudaMemcpyAsync(d_u, uc, 8 * (size_t)(row1 - row0) * (size_t)params->n_h, cudaMemcpyDeviceToDevice,
+                               stream), "copy u");
+        if (d_bits && row1 > row0)
+            CK(launch_quantize(uc, row1 - row0, params->n_h, row0, p4, params->pitch_m, d_bits, stream), "quantize");
+        return WASABI_OK;
+    }
     CK(launch_inverse(reinterpret_cast<const float2 *>(d_psi), reinterpret_cast<float2 *>(d_u), row1 - row0,
                       params->n_h, row0, params->levels, print ? p4 : nullptr, params->pitch_m, d_bits, stream),
        "inverse_wt");
@@ -536,6 +610,7 @@ wasabi_status wasabi_direct_sum(const wasabi_params *params, const void *d_dense
 
 namespace {
 struct WsLayout {
+    int64_t e0, e1;   // psi band (the band itself, or its coiflet halo band)
     size_t tables, scratch, points, bins, field, bits, total;
     size_t table_bytes, scratch_bytes, bin_bytes;
 };
@@ -545,15 +620,18 @@ wasabi_status ws_layout(const wasabi_params *P, int64_t n, int64_t row0, int64_t
     if (st != WASABI_OK) return st;
     if ((st = validate_band(P, row0, row1)) != WASABI_OK) return st;
     if (n < 0 || n > (int64_t)INT32_MAX) return fail(WASABI_EINVAL, "n out of range");
+    const int64_t Hh = wasabi_coif_halo_rows(P);
+    w.e0 = std::max<int64_t>(0, row0 - Hh);
+    w.e1 = std::min<int64_t>(P->n_h, row1 + Hh);
     w.table_bytes = g.table_bytes;
     w.scratch_bytes = g.scratch_bytes;
-    w.bin_bytes = bin_layout(g, n, row0, row1).bytes;
+    w.bin_bytes = bin_layout(g, n, w.e0, w.e1).bytes;
     size_t o = 0;
     w.tables = o; o = align_up(o + w.table_bytes, 256);
     w.scratch = o; o = align_up(o + w.scratch_bytes, 256);
     w.points = o; o = align_up(o + 16 * (size_t)n, 256);
     w.bins = o; o = align_up(o + w.bin_bytes, 256);
-    w.field = o; o = align_up(o + 8 * (size_t)(row1 - row0) * (size_t)P->n_h, 256);
+    w.field = o; o = align_up(o + 8 * (size_t)(w.e1 - w.e0) * (size_t)P->n_h, 256);
     w.bits = o; o = align_up(o + (size_t)(row1 - row0) * (size_t)(P->n_h / 8), 256);
     w.total = o;
     return WASABI_OK;
@@ -586,11 +664,16 @@ wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_pri
     if (n > 0) CK(cudaMemcpyAsync(d_pts, h_points, 16 * (size_t)n, cudaMemcpyHostToDevice, stream), "H2D points");
     if ((st = wasabi_build_psf_tables(params, ws + w.tables, w.table_bytes, ws + w.scratch, w.scratch_bytes, stream)))
         return st;
-    if ((st = wasabi_bin_points(params, ws + w.tables, d_pts, n, row0, row1, ws + w.bins, w.bin_bytes, stream)))
+    if ((st = wasabi_bin_points(params, ws + w.tables, d_pts, n, w.e0, w.e1, ws + w.bins, w.bin_bytes, stream)))
         return st;
-    if ((st = wasabi_superpose_inverse(params, ws + w.tables, ws + w.bins, row0, row1, print, h_u ? d_field : nullptr,
-                                       d_bits, stream)))
+    if (params->flags & WASABI_FLAG_COIFLET) {   // unfused: psi on the halo band, coif1 synthesis, bits
+        if ((st = wasabi_superpose(params, ws + w.tables, ws + w.bins, w.e0, w.e1, d_field, stream))) return st;
+        if ((st = wasabi_inverse_wt(params, d_field, nullptr, row0, row1, print, d_bits, stream))) return st;
+        d_field += 2 * (row0 - w.e0) * params->n_h;   // u rows [row0, row1) inside the halo band
+    } else if ((st = wasabi_superpose_inverse(params, ws + w.tables, ws + w.bins, row0, row1, print,
+                                              h_u ? d_field : nullptr, d_bits, stream))) {
         return st;
+    }
     const size_t nbits = (size_t)(row1 - row0) * (size_t)(params->n_h / 8);
     if (h_bits && nbits) CK(cudaMemcpyAsync(h_bits, d_bits, nbits, cudaMemcpyDeviceToHost, stream), "D2H bits");
     if (h_u && row1 > row0)

@@ -32,10 +32,17 @@ class Pipeline:
         tb, sb = psf_tables_bytes(p)
         self.tables = torch.empty(tb, dtype=torch.uint8, device=self.device)
         self.scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
-        self.bins = torch.empty(bin_points_bytes(p, n_max, self.row0, self.row1), dtype=torch.uint8,
+        # psi band: the band itself, or (coiflets, R-A21) the band grown by the inverse's halo rows
+        h = p.halo_rows()
+        self.e0, self.e1 = max(0, self.row0 - h), min(p.n_h, self.row1 + h)
+        self.bins = torch.empty(bin_points_bytes(p, n_max, self.e0, self.e1), dtype=torch.uint8,
                                 device=self.device)
         rows = self.row1 - self.row0
-        self.field = torch.empty((rows, p.n_h, 2), dtype=torch.float32, device=self.device)
+        if self.e0 == self.row0 and self.e1 == self.row1:
+            self.psi_band = self.field = torch.empty((rows, p.n_h, 2), dtype=torch.float32, device=self.device)
+        else:
+            self.psi_band = torch.empty((self.e1 - self.e0, p.n_h, 2), dtype=torch.float32, device=self.device)
+            self.field = self.psi_band[self.row0 - self.e0:self.row1 - self.e0]   # u rows (a view)
         self.bits = torch.empty((rows, p.n_h // 8), dtype=torch.uint8, device=self.device) if want_bits else None
         self.want_u = want_u
         self.stream = stream
@@ -51,15 +58,16 @@ class Pipeline:
         self.tables_built = True
 
     def bin(self, points):
-        bin_points(self.p, self.tables, points, self.row0, self.row1, self.bins, self.stream)
+        bin_points(self.p, self.tables, points, self.e0, self.e1, self.bins, self.stream)
 
     def superpose(self):
-        superpose(self.p, self.tables, self.bins, self.row0, self.row1, self.field, self.stream)
+        """psi on the psi band (self.psi_band; == self.field unless coiflets)."""
+        superpose(self.p, self.tables, self.bins, self.e0, self.e1, self.psi_band, self.stream)
 
     def inverse(self, fuse_bits: bool = True):
         bits = self.bits if (fuse_bits and self.bits is not None) else None
         u = self.field if self.want_u else None
-        inverse_wt(self.p, self.field, u, self.row0, self.row1, self.print_params, bits, self.stream)
+        inverse_wt(self.p, self.psi_band, u, self.row0, self.row1, self.print_params, bits, self.stream)
 
     def quantize(self):
         quantize(self.p, self.print_params, self.field, self.row0, self.row1, self.bits, self.stream)
@@ -73,7 +81,7 @@ class Pipeline:
         if build_tables or not self.tables_built:
             self.build_tables()
         self.bin(points)
-        if fused:
+        if fused and self.p.wavelet == 0:
             self.superpose_inverse()
         else:
             self.superpose()

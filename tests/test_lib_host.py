@@ -114,3 +114,24 @@ def test_no_cpu_fallback_without_gpu(W):
     s = np.zeros(sb, np.uint8)
     with pytest.raises(Exception):
         W.build_psf_tables(p, t, s, stream=0)
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", dict(levels=3)), ("C1", dict(levels=1))])
+def test_coif_host_geometry_equals_oracle(W, orc, name, kw):
+    """WASABI_FLAG_COIFLET (R-A21): the library's padded table half side, structural nnz (footprint
+    rule, written independently in C++) and N_r equal the oracle's for every depth."""
+    cfg = CONFIGS[name].replace(**kw)
+    p = W.Params.from_config(cfg, wavelet=1)
+    P = orc.Params.from_config(cfg, wavelet=1)
+    for d in range(cfg.n_depth):
+        g, o = W.depth_geometry(p, d), orc.table_info(P, d)
+        assert (g["H"], g["nnz"], g["n_r"]) == (o["H"], o["nnz"], o["n_r"]), d
+    assert p.halo_rows() == max(64, p.tile)
+
+
+@pytest.mark.parametrize("kw,msg", [(dict(levels=5), "levels <= 4"), (dict(exact=True), "EXACT_SHIFT"),
+                                    (dict(n_h=32768), "n_h <= 16384")])
+def test_coif_mode_validation(W, kw, msg):
+    p = W.Params.from_config(CONFIGS["C3"].replace(levels=3), wavelet=1, **kw)
+    with pytest.raises(W.WasabiError, match=msg):
+        W.psf_tables_bytes(p)
