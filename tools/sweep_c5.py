@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--aligned", action="store_true")
     ap.add_argument("--exact", action="store_true", help="offset-class tables (WASABI_FLAG_EXACT_SHIFT, R-A20)")
     ap.add_argument("--levels", type=int, default=None)
+    ap.add_argument("--wavelet", type=int, default=0, help="1: coif1 tables (WASABI_FLAG_COIFLET, R-A21)")
     ap.add_argument("--depths", type=int, default=None)
     ap.add_argument("--out", default="gpurun_out/c5_sweep.jsonl")
     a = ap.parse_args()
@@ -56,32 +57,29 @@ def main():
         t_direct = None
         for r in [float(x) for x in a.rs.split(",")]:
             cfg = base.replace(retention=r)
-            p = W.Params.from_config(cfg, exact=a.exact)
+            p = W.Params.from_config(cfg, exact=a.exact, wavelet=a.wavelet)
             pl = W.Pipeline(p, n, 0, p.n_h)
             t_w = timed(lambda: pl.run(d_pts), reps=3 if n < 10_000_000 else 1)
             if u_ref is None:
-                # the reference uses standard-mode bins (whole PSF footprints at r <= 1)
-                if a.exact:
-                    ps = W.Params.from_config(cfg.replace(retention=1.0))
-                    pls = W.Pipeline(ps, n, 0, ps.n_h, want_bits=False)
-                    pls.build_tables()
-                    pls.bin(d_pts)
-                    bins_ref = pls.bins
-                else:
-                    bins_ref = pl.bins
+                # the reference stamps whole PSFs: bins of the standard mode at r = 1 (R-A19's reach of
+                # a smaller r may not cover the PSF's edge)
+                ps = W.Params.from_config(cfg.replace(retention=1.0))
+                pls = W.Pipeline(ps, n, 0, ps.n_h, want_bits=False)
+                pls.build_tables()
+                pls.bin(d_pts)
+                bins_ref = pls.bins
                 dense = torch.empty(W.psf_dense_bytes(p), dtype=torch.uint8, device="cuda")
                 W.build_psf_dense(p, dense)
                 u_ref = torch.empty_like(pl.field)
                 t_direct = timed(lambda: W.direct_sum(p, dense, bins_ref, 0, p.n_h, u_ref), reps=1)
-                del dense, bins_ref
-                if a.exact:
-                    del pls
+                del dense, bins_ref, pls
             diff = (pl.field - u_ref).double()
             mse = float((diff * diff).sum(dim=-1).mean())
             peak = float((u_ref.double() ** 2).sum(dim=-1).max())
             psnr = 10 * math.log10(peak / mse) if mse > 0 else float("inf")
             st = W.bins_stats(pl.bins)
-            rec = {"n_points": n, "retention": r, "aligned": a.aligned, "exact": a.exact, "levels": cfg.levels,
+            rec = {"n_points": n, "retention": r, "aligned": a.aligned, "exact": a.exact, "wavelet": a.wavelet,
+                   "levels": cfg.levels,
                    "n_depth": cfg.n_depth, "wasabi_ms": t_w,
                    "gpix_per_s": p.n_h ** 2 / (t_w * 1e-3) / 1e9, "points_per_s": n / (t_w * 1e-3),
                    "direct_sum_ms": t_direct, "speedup_vs_direct": t_direct / t_w, "psnr_db_vs_direct": psnr,
