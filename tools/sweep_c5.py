@@ -68,10 +68,10 @@ def main():
                 pls.build_tables()
                 pls.bin(d_pts)
                 bins_ref = pls.bins
-                dense = torch.empty(W.psf_dense_bytes(p), dtype=torch.uint8, device="cuda")
-                W.build_psf_dense(p, dense)
+                dense = torch.empty(W.psf_dense_bytes(ps), dtype=torch.uint8, device="cuda")
+                W.build_psf_dense(ps, dense)
                 u_ref = torch.empty_like(pl.field)
-                t_direct = timed(lambda: W.direct_sum(p, dense, bins_ref, 0, p.n_h, u_ref), reps=1)
+                t_direct = timed(lambda: W.direct_sum(ps, dense, bins_ref, 0, ps.n_h, u_ref), reps=1)
                 del dense, bins_ref, pls
             diff = (pl.field - u_ref).double()
             mse = float((diff * diff).sum(dim=-1).mean())
