@@ -160,9 +160,10 @@ cudaError_t launch_bin(const BinHeader &bh, void *d_bins, const KDesc *kd, const
 
 // fused = 0: write psi; fused = 1: inverse Haar in shared memory, write u (psi pointer, may be NULL)
 // and, if bits != NULL, the print bits (print4 = {xr, yr, zr, 1/lambda}).
+// tile rows [tile_row0, tile_row1) of the bins' band (tile_row1 < 0: all)
 cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int cls_bits, int tiles_x,
                              int tiles_y, int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4,
-                             double pitch, uint8_t *bits, cudaStream_t s);
+                             double pitch, uint8_t *bits, cudaStream_t s, int tile_row0 = 0, int tile_row1 = -1);
 cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStream_t s);
 
 cudaError_t launch_psf_dense(const DenseDesc *d_desc, int n_depth, float2 *out, double k, double pitch,

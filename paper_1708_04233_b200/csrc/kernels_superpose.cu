@@ -32,6 +32,7 @@ namespace {
 struct SupArgs {
     int L, cls_bits, tiles_x;
     int64_t row0, n_h;
+    int64_t tile0;   // first tile (row-major in the bins' band) of this launch
 };
 
 #ifndef WASABI_KD
@@ -39,6 +40,9 @@ struct SupArgs {
 #endif
 #ifndef WASABI_MINB
 #define WASABI_MINB 6
+#endif
+#ifndef WASABI_BATCH_OUTER
+#define WASABI_BATCH_OUTER 0
 #endif
 #ifndef WASABI_PF
 #define WASABI_PF 0   // bulk L2 prefetch of each batch's ranges: measured slower with the ring at full C4
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cls = wid & 1, strip = wid >> 1;
-    const int64_t t = blockIdx.x;
+    const int64_t t = A.tile0 + blockIdx.x;
     const int tile_x0 = (int)(t % A.tiles_x) * T;
     const int tile_y0 = (int)(A.row0 + (t / A.tiles_x) * (int64_t)T);
     const int strip_y0 = tile_y0 + kWinRows * strip;
@@ -196,8 +200,13 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     auto next_range = [&]() {
         while (gm == 0u) {
             if (++gj >= 4) {
+#if WASABI_BATCH_OUTER
+                have = false;        // the outer loop loads the next batch (one inlined copy)
+                return;
+#else
                 if (!load_batch()) { have = false; return; }
                 gj = 0;
+#endif
             }
             select_slot();
         }
@@ -251,6 +260,11 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         sts2(sa, o);                                                                \
     } while (0)
 #pragma unroll
+#if WASABI_BATCH_OUTER
+    bool batch = have;
+    while (batch) {
+#endif
+#pragma unroll
     for (int u = 0; u < kD; u++) WASABI_PREFETCH(u);
     bool more = true;
     while (more) {
@@ -261,6 +275,15 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             WASABI_PREFETCH(u);
         }
     }
+#if WASABI_BATCH_OUTER
+    batch = load_batch();
+    if (batch) {
+        gj = 0;
+        select_slot();
+        next_range();
+    }
+    }
+#endif
 #undef WASABI_PREFETCH
 #undef WASABI_CONSUME
     __syncthreads();
@@ -308,11 +331,13 @@ cudaError_t launch_t(const void *d_bins, const void *d_tables, const SupArgs &A,
 
 cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int cls_bits, int tiles_x,
                              int tiles_y, int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4,
-                             double pitch, uint8_t *bits, cudaStream_t s) {
+                             double pitch, uint8_t *bits, cudaStream_t s, int tile_row0, int tile_row1) {
     if (S != T + kWinMargin) return cudaErrorInvalidValue;
+    if (tile_row1 < 0) tile_row1 = tiles_y;
     SupArgs A;
     A.L = L; A.cls_bits = cls_bits; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
-    const int64_t n_tiles = (int64_t)tiles_x * tiles_y;
+    A.tile0 = (int64_t)tile_row0 * tiles_x;
+    const int64_t n_tiles = (int64_t)tiles_x * (tile_row1 - tile_row0);
     const QArgs qa = make_qargs(print4, pitch, n_h);
     if (cls_bits)
         return T <= 64 ? launch_t<64, true>(d_bins, d_tables, A, n_tiles, psi, fused, qa, bits, s)

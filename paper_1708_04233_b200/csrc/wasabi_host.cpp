@@ -661,25 +661,63 @@ wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_pri
     float *d_pts = reinterpret_cast<float *>(ws + w.points);
     float *d_field = reinterpret_cast<float *>(ws + w.field);
     uint8_t *d_bits = reinterpret_cast<uint8_t *>(ws + w.bits);
-    if (n > 0) CK(cudaMemcpyAsync(d_pts, h_points, 16 * (size_t)n, cudaMemcpyHostToDevice, stream), "H2D points");
+    // A side stream carries the copies: the points' H2D overlaps the table build, and the bits / u
+    // of each row chunk go to the host while the next chunk is superposed (PCIe under the compute).
+    cudaStream_t cs = nullptr;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
+    struct Guard {
+        cudaStream_t s;
+        ~Guard() { cudaStreamDestroy(s); }   // released once its pending work completes
+    } guard{cs};
+    auto join = [&](cudaStream_t waiter, cudaStream_t waited) -> cudaError_t {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (r != cudaSuccess) return r;
+        r = cudaEventRecord(e, waited);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(waiter, e, 0);
+        cudaEventDestroy(e);
+        return r;
+    };
+    CK(join(cs, stream), "order copy stream");
+    if (n > 0) CK(cudaMemcpyAsync(d_pts, h_points, 16 * (size_t)n, cudaMemcpyHostToDevice, cs), "H2D points");
     if ((st = wasabi_build_psf_tables(params, ws + w.tables, w.table_bytes, ws + w.scratch, w.scratch_bytes, stream)))
         return st;
+    CK(join(stream, cs), "wait for points");
     if ((st = wasabi_bin_points(params, ws + w.tables, d_pts, n, w.e0, w.e1, ws + w.bins, w.bin_bytes, stream)))
         return st;
+    const size_t bpr = (size_t)(params->n_h / 8), upr = 8 * (size_t)params->n_h;   // bytes per row
     if (params->flags & WASABI_FLAG_COIFLET) {   // unfused: psi on the halo band, coif1 synthesis, bits
         if ((st = wasabi_superpose(params, ws + w.tables, ws + w.bins, w.e0, w.e1, d_field, stream))) return st;
         if ((st = wasabi_inverse_wt(params, d_field, nullptr, row0, row1, print, d_bits, stream))) return st;
         d_field += 2 * (row0 - w.e0) * params->n_h;   // u rows [row0, row1) inside the halo band
-    } else if ((st = wasabi_superpose_inverse(params, ws + w.tables, ws + w.bins, row0, row1, print,
-                                              h_u ? d_field : nullptr, d_bits, stream))) {
-        return st;
+        CK(join(cs, stream), "wait for u");
+        if (h_bits && row1 > row0)
+            CK(cudaMemcpyAsync(h_bits, d_bits, bpr * (size_t)(row1 - row0), cudaMemcpyDeviceToHost, cs), "D2H bits");
+        if (h_u && row1 > row0)
+            CK(cudaMemcpyAsync(h_u, d_field, upr * (size_t)(row1 - row0), cudaMemcpyDeviceToHost, cs), "D2H u");
+    } else if (row1 > row0) {
+        const int T = params->tile;
+        const int tiles_y = (int)((row1 - row0) / T);
+        const int chunk = std::max(1, (tiles_y + 7) / 8);   // 8 row chunks
+        double p4[4] = {print->x_r_m, print->y_r_m, print->z_r_m, 1.0 / params->wavelength_m};
+        for (int ty = 0; ty < tiles_y; ty += chunk) {
+            const int ty1 = std::min(tiles_y, ty + chunk);
+            CK(launch_superpose(ws + w.bins, ws + w.tables, T, T + kWinMargin, params->levels, cls_bits(*params),
+                                (int)(params->n_h / T), tiles_y, row0, params->n_h,
+                                h_u ? reinterpret_cast<float2 *>(d_field) : nullptr, 1, p4, params->pitch_m, d_bits,
+                                stream, ty, ty1),
+               "superpose_inverse chunk");
+            CK(join(cs, stream), "chunk done");
+            const size_t r0 = (size_t)ty * T, nr = (size_t)(ty1 - ty) * T;
+            if (h_bits) CK(cudaMemcpyAsync(h_bits + r0 * bpr, d_bits + r0 * bpr, nr * bpr, cudaMemcpyDeviceToHost, cs),
+                           "D2H bits");
+            if (h_u)
+                CK(cudaMemcpyAsync(reinterpret_cast<char *>(h_u) + r0 * upr,
+                                   reinterpret_cast<char *>(d_field) + r0 * upr, nr * upr, cudaMemcpyDeviceToHost, cs),
+                   "D2H u");
+        }
     }
-    const size_t nbits = (size_t)(row1 - row0) * (size_t)(params->n_h / 8);
-    if (h_bits && nbits) CK(cudaMemcpyAsync(h_bits, d_bits, nbits, cudaMemcpyDeviceToHost, stream), "D2H bits");
-    if (h_u && row1 > row0)
-        CK(cudaMemcpyAsync(h_u, d_field, 8 * (size_t)(row1 - row0) * (size_t)params->n_h, cudaMemcpyDeviceToHost,
-                           stream),
-           "D2H u");
+    CK(join(stream, cs), "join copy stream");   // the caller's stream covers every copy
     return WASABI_OK;
 }
 
