@@ -117,12 +117,53 @@ __global__ void __launch_bounds__(256) scatter_kernel(BinArgs A, const KDesc *__
     }
 }
 
-// Warp-per-tile bitonic sort for bins of <= 1024 entries; larger bins are queued.
+// Warp-per-tile bitonic sort for bins of <= 1024 entries, in registers: element i = 32 e + lane
+// (E = m / 32 per lane, m = the next power of two >= max(n, 32)); stages with partner distance
+// j < 32 exchange through shuffles, j >= 32 between a lane's own registers.  Larger bins are queued.
 constexpr int kSmallBin = 1024;
+template <int E>
+__device__ __forceinline__ void warp_sort_bin(uint32_t *__restrict__ idx, unsigned long long b, int n, int lane) {
+    uint32_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int i = 32 * e + lane;
+        v[e] = i < n ? idx[b + i] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const int p = e ^ (j >> 5);
+                    if (p > e) {
+                        const bool up = ((32 * e + lane) & k) == 0;
+                        const uint32_t x = v[e], y = v[p];
+                        if ((x > y) == up) { v[e] = y; v[p] = x; }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[e], j);
+                    const bool up = ((32 * e + lane) & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    v[e] = (lower == up) ? min(v[e], o) : max(v[e], o);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int i = 32 * e + lane;
+        if (i < n) idx[b + i] = v[e];
+    }
+}
+
 __global__ void __launch_bounds__(256) sort_small_kernel(int64_t n_tiles, const unsigned long long *__restrict__ ptr,
                                                          uint32_t *__restrict__ idx, uint32_t *__restrict__ big_list,
                                                          unsigned int *big_count) {
-    __shared__ uint32_t sh[8][kSmallBin];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t t = (int64_t)blockIdx.x * 8 + w;
     if (t >= n_tiles) return;
@@ -133,24 +174,12 @@ __global__ void __launch_bounds__(256) sort_small_kernel(int64_t n_tiles, const 
         if (lane == 0) big_list[atomicAdd(big_count, 1u)] = (uint32_t)t;
         return;
     }
-    int m = 2;
-    while (m < n) m <<= 1;
-    uint32_t *s = sh[w];
-    for (int i = lane; i < m; i += 32) s[i] = i < n ? idx[b + i] : 0xffffffffu;
-    __syncwarp();
-    for (int k = 2; k <= m; k <<= 1)
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-            for (int i = lane; i < m; i += 32) {
-                const int l = i ^ jj;
-                if (l > i) {
-                    const uint32_t x = s[i], y = s[l];
-                    const bool up = (i & k) == 0;
-                    if ((x > y) == up) { s[i] = y; s[l] = x; }
-                }
-            }
-            __syncwarp();
-        }
-    for (int i = lane; i < n; i += 32) idx[b + i] = s[i];
+    if (n <= 32) warp_sort_bin<1>(idx, b, n, lane);
+    else if (n <= 64) warp_sort_bin<2>(idx, b, n, lane);
+    else if (n <= 128) warp_sort_bin<4>(idx, b, n, lane);
+    else if (n <= 256) warp_sort_bin<8>(idx, b, n, lane);
+    else if (n <= 512) warp_sort_bin<16>(idx, b, n, lane);
+    else warp_sort_bin<32>(idx, b, n, lane);
 }
 
 // Large bins: one CTA per queued tile; 4096-entry chunks sorted in shared memory, then merge

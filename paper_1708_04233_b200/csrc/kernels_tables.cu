@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(256) select_hist_kernel(const void *tables, co
     const int X0 = (local % D.tiles) * kTile, Y0 = (local / D.tiles) * kTile;
     const int side = D.side;
     const SelState s = st[d];
+    if (s.k == 0) return;   // this depth's threshold is already exact (select_pick_kernel)
     const int shift = 56 - 8 * pass;
     sh[threadIdx.x] = 0;
     __syncthreads();
@@ -152,17 +153,21 @@ __global__ void select_pick_kernel(unsigned int *hist, SelState *st, int n_depth
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_depth) return;
     SelState s = st[d];
+    if (s.k == 0) return;   // done in an earlier pass
     const int shift = 56 - 8 * pass;
-    unsigned long long cum = 0;
+    unsigned long long cum = 0, cnt = 0;
     int digit = 0;
     for (int b = 255; b >= 0; b--) {
         const unsigned long long c = hist[d * 256 + b];
-        if (cum + c >= s.k) { digit = b; break; }
+        if (cum + c >= s.k) { digit = b; cnt = c; break; }
         cum += c;
     }
     s.k -= cum;
     s.prefix |= (unsigned long long)digit << shift;
     s.mask |= 0xFFull << shift;
+    // every key under the new prefix is kept: key >= prefix (lower digits 0) is already the exact
+    // top-N_r set, so the remaining passes skip this depth (k = 0 marks it)
+    if (cnt == s.k) s.k = 0;
     st[d] = s;
     for (int b = 0; b < 256; b++) hist[d * 256 + b] = 0;
 }
