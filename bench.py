@@ -59,7 +59,7 @@ def oracle_sample(cfg, pts, window=None, table_depths=None, setup=None):
         setup = {}
         geo = O.geometry(P)
         setup["area"] = [(2 * int(h)) ** 2 for h in geo["H"]]
-        w = window or min(cfg.n_h, 4096)
+        w = window or min(cfg.n_h, 6144)
         x0 = y0 = cfg.n_h // 2 - w // 2
         ix, iy, iz, ok = O.points(P, pts)
         E = geo["E"][iz]

@@ -103,6 +103,10 @@ __global__ void write_blob_kernel(unsigned char *dst, Blob b) {
 // Asynchronous, graph-capturable host->device copy of small descriptors through kernel parameters
 // (no pageable-memcpy stream synchronisation).
 cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    // large descriptor arrays (thousands of offset-class tables): one stream-ordered copy from the
+    // (pageable) host array instead of hundreds of parameter-blob launches; the call returns once
+    // the source has been staged, so the caller may free it
+    if (bytes > 16384) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
     const unsigned char *p = static_cast<const unsigned char *>(src);
     unsigned char *d = static_cast<unsigned char *>(dst);
     for (size_t off = 0; off < bytes; off += sizeof(Blob::data)) {

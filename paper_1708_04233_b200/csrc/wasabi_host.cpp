@@ -13,6 +13,8 @@
 #include "internal.h"
 
 #include <atomic>
+#include <memory>
+#include <mutex>
 
 using namespace wasabi;
 
@@ -176,7 +178,7 @@ double level_z(const wasabi_params &P, double dz, int d) {
     return P.z_min_m + (double)d * dz;
 }
 
-wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
+wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
     wasabi_status st = validate(P);
     if (st != WASABI_OK) return st;
     g.P = *P;
@@ -291,6 +293,39 @@ wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
         g.sc_pre = so; so = align_up(so + 8 * g.pre.size(), 256);
     }
     g.scratch_bytes = so;
+    return WASABI_OK;
+}
+
+// Every entry point derives the geometry from the parameters; the structural nnz counts make that
+// O(table area) host work (tens of ms for 4^L offset-class or coiflet tables), so the last few
+// parameter sets are memoised (keyed by the full parameter bytes).
+struct GeoCache {
+    std::mutex mu;
+    std::vector<std::pair<wasabi_params, std::shared_ptr<const Geo>>> items;   // most recent last
+};
+GeoCache &geo_cache() {
+    static GeoCache c;
+    return c;
+}
+
+wasabi_status compute_geo(const wasabi_params *P, Geo &g) {
+    wasabi_status st = validate(P);
+    if (st != WASABI_OK) return st;
+    GeoCache &c = geo_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto &it : c.items)
+            if (std::memcmp(&it.first, P, sizeof *P) == 0) {
+                g = *it.second;
+                return WASABI_OK;
+            }
+    }
+    auto fresh = std::make_shared<Geo>();
+    if ((st = compute_geo_uncached(P, *fresh)) != WASABI_OK) return st;
+    g = *fresh;
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.items.emplace_back(*P, fresh);
+    if (c.items.size() > 8) c.items.erase(c.items.begin());
     return WASABI_OK;
 }
 
