@@ -7,9 +7,9 @@
 //   step 1: psf_f64_kernel (PSF into an fp64 work table), fb_fwd_pass_kernel (per level: rows A->B,
 //           columns B->A, fp64, taps summed in order k = 0..5 with _rn operations -- the same IEEE
 //           sequence as the specification, so the fp32 rank keys match bit for bit), coef_keys_kernel.
-//   step 3: fb_inv_line_kernel: per level (L..1) columns then rows, in place on the psi band that
-//           carries a halo of kCoifHalo rows (one CTA per line; the line's level samples in shared
-//           memory; fp32).  Samples outside the band / hologram are zero (R-A21 boundary).
+//   step 3: fb_inv_cols_kernel / fb_inv_rows_kernel: per level (L..1) columns then rows, in place on
+//           the psi band that carries a halo of one tile row (rolling window of pairs along the lines
+//           in shared memory; fp32).  Samples outside the band / hologram are zero (R-A21 boundary).
 // Off the fused hot path: the coiflet inverse is not block-local, so this mode runs superpose on the
 // halo band, then the line passes, then quantise.
 #include <cuda_runtime.h>
@@ -119,35 +119,86 @@ __global__ void __launch_bounds__(256) coef_keys_kernel(const double2 *__restric
     key[i] = __float_as_uint(__double2float_rn(__dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y))));
 }
 
-// One synthesis pass of level l on the band psi (rows x n_h, in place): CTA = line.  rows = 0:
-// line = column X = s j, samples along Y; rows = 1: line = row Y = s j.
-__global__ void __launch_bounds__(256) fb_inv_line_kernel(float2 *__restrict__ psi, int64_t nrows, int64_t n_h, int l,
-                                                          int rows, Filt F) {
-    extern __shared__ float2 line[];
-    const int s = 1 << (l - 1);
-    const int j = blockIdx.x;
-    const int64_t len = rows ? n_h : nrows;
-    const int N = (int)(len / s);
-    auto idx = [&](int n) -> int64_t {
-        return rows ? (int64_t)(s * j) * n_h + (int64_t)s * n : (int64_t)s * n * n_h + (int64_t)s * j;
-    };
-    for (int n = threadIdx.x; n < N; n += blockDim.x) line[n] = psi[idx(n)];
-    __syncthreads();
+// One synthesis pass of level l on the band psi (nrows x n_h, in place), as a rolling window along
+// the lines.  Output samples 2p and 2p + 1 need pairs p - 1, p, p + 1 (pair m = samples 2m, 2m + 1;
+// k = n - 2m + 2 in [0, 5]); a CTA owns its lines, loads blocks of kBP pairs, keeps the last two
+// pairs of the previous block, and writes outputs only over pairs it has already read: in place
+// without races.  Columns: 32 adjacent lines per CTA (coalesced across lines); rows: one line per
+// CTA with the threads along it.  Samples beyond the band / hologram are zero (R-A21).
+constexpr int kBP = 32;
+
+__device__ __forceinline__ float2 synth(const float2 *a, const float2 *d, int q, int stride, const float *h0,
+                                        const float *h1, int odd) {
+    // pairs q - 1, q, q + 1 of the window (p - 1, p, p + 1), k = 4, 2, 0 (even) / 5, 3, 1 (odd)
+    float2 x = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+        const int k = 4 - 2 * t + odd;
+        const float2 A = a[(q + t) * stride], D = d[(q + t) * stride];
+        x.x = fmaf(h0[k], A.x, fmaf(h1[k], D.x, x.x));
+        x.y = fmaf(h0[k], A.y, fmaf(h1[k], D.y, x.y));
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(256) fb_inv_cols_kernel(float2 *__restrict__ psi, int64_t nrows, int64_t n_h, int l,
+                                                          Filt F) {
+    __shared__ float2 sa[kBP + 2][32], sd[kBP + 2][32];
+    const int s = 1 << (l - 1), tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int ncol = (int)(n_h / s), np = (int)(nrows / s) / 2;
+    const int j = blockIdx.x * 32 + tx;
+    const bool colok = j < ncol;
     float h0[6], h1[6];
 #pragma unroll
     for (int k = 0; k < 6; k++) { h0[k] = (float)F.h0[k]; h1[k] = (float)F.h1[k]; }
-    for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        float xr = 0.f, xi = 0.f;
-        const int m_hi = (n + 2) >> 1;
-#pragma unroll
-        for (int q = 0; q < 3; q++) {
-            const int m = m_hi - q, k = n - 2 * m + 2;
-            if (m < 0 || 2 * m + 1 >= N || k < 0 || k > 5) continue;
-            const float2 a = line[2 * m], d = line[2 * m + 1];
-            xr = fmaf(h0[k], a.x, fmaf(h1[k], d.x, xr));
-            xi = fmaf(h0[k], a.y, fmaf(h1[k], d.y, xi));
+    auto at = [&](int n) -> int64_t { return (int64_t)s * n * n_h + (int64_t)s * j; };
+    if (ty < 2) { sa[ty][tx] = make_float2(0.f, 0.f); sd[ty][tx] = make_float2(0.f, 0.f); }   // pairs -2, -1
+    for (int p0 = 0; p0 <= np; p0 += kBP) {
+        for (int q = ty; q < kBP; q += 8) {           // pairs p0 .. p0 + kBP - 1 -> window rows 2..
+            const int p = p0 + q;
+            float2 A = make_float2(0.f, 0.f), D = A;
+            if (colok && p < np) { A = psi[at(2 * p)]; D = psi[at(2 * p + 1)]; }
+            sa[q + 2][tx] = A; sd[q + 2][tx] = D;
         }
-        psi[idx(n)] = make_float2(xr, xi);
+        __syncthreads();
+        // outputs for pairs p = p0 - 1 + q (window rows q .. q + 2 hold p - 1 .. p + 1)
+        for (int q = ty; q < kBP; q += 8) {
+            const int p = p0 - 1 + q;
+            if (!colok || p < 0 || p >= np) continue;
+            psi[at(2 * p)] = synth(&sa[0][tx], &sd[0][tx], q, 32, h0, h1, 0);
+            psi[at(2 * p + 1)] = synth(&sa[0][tx], &sd[0][tx], q, 32, h0, h1, 1);
+        }
+        __syncthreads();
+        if (ty < 2) { sa[ty][tx] = sa[kBP + ty][tx]; sd[ty][tx] = sd[kBP + ty][tx]; }
+        __syncthreads();
+    }
+}
+
+constexpr int kRP = 256;
+__global__ void __launch_bounds__(256) fb_inv_rows_kernel(float2 *__restrict__ psi, int64_t nrows, int64_t n_h, int l,
+                                                          Filt F) {
+    __shared__ float2 sa[kRP + 2], sd[kRP + 2];
+    const int s = 1 << (l - 1), t = threadIdx.x;
+    const int np = (int)(n_h / s) / 2;
+    const int64_t row = (int64_t)s * blockIdx.x * n_h;
+    float h0[6], h1[6];
+#pragma unroll
+    for (int k = 0; k < 6; k++) { h0[k] = (float)F.h0[k]; h1[k] = (float)F.h1[k]; }
+    if (t < 2) { sa[t] = make_float2(0.f, 0.f); sd[t] = make_float2(0.f, 0.f); }
+    for (int p0 = 0; p0 <= np; p0 += kRP) {
+        const int p = p0 + t;
+        float2 A = make_float2(0.f, 0.f), D = A;
+        if (p < np) { A = psi[row + (int64_t)s * (2 * p)]; D = psi[row + (int64_t)s * (2 * p + 1)]; }
+        sa[t + 2] = A; sd[t + 2] = D;
+        __syncthreads();
+        const int po = p0 - 1 + t;
+        if (po >= 0 && po < np) {
+            psi[row + (int64_t)s * (2 * po)] = synth(sa, sd, t, 1, h0, h1, 0);
+            psi[row + (int64_t)s * (2 * po + 1)] = synth(sa, sd, t, 1, h0, h1, 1);
+        }
+        __syncthreads();
+        if (t < 2) { sa[t] = sa[kRP + t]; sd[t] = sd[kRP + t]; }
+        __syncthreads();
     }
 }
 
@@ -188,16 +239,12 @@ cudaError_t launch_coif_tables(const TableHeader &h, const void *d_tables, doubl
 
 cudaError_t launch_coif_inverse(float2 *psi, int64_t nrows, int64_t n_h, int L, cudaStream_t s) {
     const Filt F = coif1();
-    const int max_len = (int)(nrows > n_h ? nrows : n_h);
-    const int smem = max_len * (int)sizeof(float2);
-    cudaError_t e = cudaFuncSetAttribute(fb_inv_line_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
     for (int l = L; l >= 1; l--) {
         const int sgrid = 1 << (l - 1);
         const unsigned ncols = (unsigned)(n_h / sgrid), nrow = (unsigned)(nrows / sgrid);
         count_launches(2);
-        fb_inv_line_kernel<<<ncols, 256, (int)(nrows / sgrid) * (int)sizeof(float2), s>>>(psi, nrows, n_h, l, 0, F);
-        fb_inv_line_kernel<<<nrow, 256, (int)(n_h / sgrid) * (int)sizeof(float2), s>>>(psi, nrows, n_h, l, 1, F);
+        fb_inv_cols_kernel<<<(ncols + 31) / 32, 256, 0, s>>>(psi, nrows, n_h, l, F);
+        fb_inv_rows_kernel<<<nrow, 256, 0, s>>>(psi, nrows, n_h, l, F);
     }
     return cudaGetLastError();
 }
