@@ -47,6 +47,29 @@ struct SupArgs {
 
 constexpr int kD = WASABI_KD;          // register ring depth (chunks in flight per warp)
 
+#ifndef WASABI_L1NA
+#define WASABI_L1NA 0
+#endif
+// Window-LUT loads: read once per use (14% L1 hit rate), so optionally not allocated in L1.
+__device__ __forceinline__ float2 ldg_stream(const float2 *p) {
+#if WASABI_L1NA
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ int ldg_stream(const uint16_t *p) {
+#if WASABI_L1NA
+    unsigned short v;
+    asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // Bulk prefetch of [p, p + bytes) into L2 (16-byte granules): one instruction per range, so the
 // later chunks of a range hit L2 instead of waiting on DRAM.
 __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
@@ -233,8 +256,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         const bool v = have && e < c_end;                                           \
         rp[u] = 0;                                                                  \
         if (v) {                                                                    \
-            rv[u] = __ldg(vval + e);                                                \
-            rp[u] = __ldg(vpos + e);                                                \
+            rv[u] = ldg_stream(vval + e);                                           \
+            rp[u] = ldg_stream(vpos + e);                                           \
         }                                                                           \
         rb[u] = v ? c_sa : dummy_sa;                                                \
         ra[u] = c_a;                                                                \
