@@ -141,7 +141,8 @@ cudaError_t launch_select(const TableHeader &h, const void *d_tables, const uint
                           unsigned int *hist, unsigned long long *sel_state, int n_depth, cudaStream_t s);
 cudaError_t launch_groups(const TableHeader &h, void *d_tables, const float2 *coef_val, const uint32_t *coef_key,
                           const unsigned long long *sel_state, int pass, cudaStream_t s);
-cudaError_t launch_vgroups(const TableHeader &h, void *d_tables, int pass, cudaStream_t s);
+// the window LUT per canonical entry (pass 0: count into the vptr slots; pass 1: place at cursor[])
+cudaError_t launch_ventries(const TableHeader &h, void *d_tables, int pass, int32_t *cursor, cudaStream_t s);
 // coiflet mode (R-A21): fp64 PSF + L-level coif1 analysis of every table (work/tmp: fp64 tables,
 // d_pre: per level the (n_tables + 1) prefix of (lines x pairs) work items, h_pre_last: its totals)
 cudaError_t launch_coif_tables(const TableHeader &h, const void *d_tables, double2 *work, double2 *tmp,

@@ -62,32 +62,50 @@ __device__ __forceinline__ int sq_gap(int i, int t0, int T) {
     return g * g;
 }
 
+// The tiles of a point's footprint (R-A19): the square [ix - Ek, ix + Ek]^2 clipped to the band,
+// then the squared-distance test.  Warp-cooperative: the 32 points of a warp are taken one at a time
+// and the lanes walk that point's tile box (a footprint is ~10 x 10 tiles at C4), so the atomics of
+// a point are issued in parallel instead of one after the other by one thread.
+template <typename F>
+__device__ __forceinline__ void warp_footprint(int4 q, bool valid, const KDesc *__restrict__ kd, const BinArgs &A,
+                                               int lane, F &&f) {
+    unsigned vm = __ballot_sync(0xffffffffu, valid);
+    while (vm) {
+        const int src = __ffs(vm) - 1;
+        vm &= vm - 1u;
+        const int ix = __shfl_sync(0xffffffffu, q.x, src), iy = __shfl_sync(0xffffffffu, q.y, src);
+        const int iz = __shfl_sync(0xffffffffu, q.z, src);
+        const int tb = table_of(ix, iy, iz, A.cls_bits);
+        const int Q = __ldg(&kd[tb].Q);
+        int tx0, tx1, ty0, ty1;
+        tile_range(ix, iy, __ldg(&kd[tb].Ek), A, tx0, tx1, ty0, ty1);
+        const int w = tx1 - tx0 + 1, nbox = w * (ty1 - ty0 + 1);
+        for (int i = lane; i < nbox; i += 32) {
+            const int ty = ty0 + i / w, tx = tx0 + i % w;
+            const int rem = Q - sq_gap(iy, (int)A.row0 + ty * A.T, A.T);
+            if (rem >= 0 && sq_gap(ix, tx * A.T, A.T) <= rem) f((int64_t)ty * A.tiles_x + tx, src);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) convert_count_kernel(const float4 *__restrict__ pts, BinArgs A,
                                                             const KDesc *__restrict__ kd, int4 *__restrict__ pout,
                                                             uint32_t *__restrict__ cnt, BinHeader *bh) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool valid = false;
+    int4 q = make_int4(0, 0, -1, 0);
     if (j < A.n) {
         const float4 p = pts[j];
         int ix = 0, iy = 0, iz = 0;
         valid = convert_point(p, A, ix, iy, iz);
-        pout[j] = make_int4(ix, iy, valid ? iz : -1, __float_as_int(p.w));
-        if (valid) {
-            int tx0, tx1, ty0, ty1;
-            const int tb = table_of(ix, iy, iz, A.cls_bits);
-            const int Q = kd[tb].Q;
-            tile_range(ix, iy, kd[tb].Ek, A, tx0, tx1, ty0, ty1);
-            for (int ty = ty0; ty <= ty1; ty++) {
-                const int rem = Q - sq_gap(iy, (int)A.row0 + ty * A.T, A.T);
-                if (rem < 0) continue;
-                for (int tx = tx0; tx <= tx1; tx++)
-                    if (sq_gap(ix, tx * A.T, A.T) <= rem) atomicAdd(&cnt[(int64_t)ty * A.tiles_x + tx], 1u);
-            }
-        }
+        q = make_int4(ix, iy, valid ? iz : -1, __float_as_int(p.w));
+        pout[j] = q;
     }
+    const int lane = threadIdx.x & 31;
+    warp_footprint(q, valid, kd, A, lane, [&](int64_t t, int) { atomicAdd(&cnt[t], 1u); });
     const unsigned vb = __ballot_sync(0xffffffffu, valid);
     const unsigned ib = __ballot_sync(0xffffffffu, j < A.n && !valid);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         if (vb) atomicAdd(&bh->n_valid, (unsigned long long)__popc(vb));
         if (ib) atomicAdd(&bh->n_skipped, (unsigned long long)__popc(ib));
     }
@@ -98,23 +116,12 @@ __global__ void __launch_bounds__(256) scatter_kernel(BinArgs A, const KDesc *__
                                                       const unsigned long long *__restrict__ ptr,
                                                       uint32_t *__restrict__ fill, uint32_t *__restrict__ idx) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= A.n) return;
-    const int4 q = pconv[j];
-    if (q.z < 0) return;
-    int tx0, tx1, ty0, ty1;
-    const int tb = table_of(q.x, q.y, q.z, A.cls_bits);
-    const int Q = kd[tb].Q;
-    tile_range(q.x, q.y, kd[tb].Ek, A, tx0, tx1, ty0, ty1);
-    for (int ty = ty0; ty <= ty1; ty++) {
-        const int rem = Q - sq_gap(q.y, (int)A.row0 + ty * A.T, A.T);
-        if (rem < 0) continue;
-        for (int tx = tx0; tx <= tx1; tx++) {
-            if (sq_gap(q.x, tx * A.T, A.T) > rem) continue;
-            const int64_t t = (int64_t)ty * A.tiles_x + tx;
-            const uint32_t slot = atomicAdd(&fill[t], 1u);
-            idx[ptr[t] + slot] = (uint32_t)j;
-        }
-    }
+    const int4 q = j < A.n ? pconv[j] : make_int4(0, 0, -1, 0);
+    const int64_t j0 = j - (threadIdx.x & 31);           // point index of lane 0
+    warp_footprint(q, q.z >= 0, kd, A, threadIdx.x & 31, [&](int64_t t, int src) {
+        const uint32_t slot = atomicAdd(&fill[t], 1u);
+        idx[ptr[t] + slot] = (uint32_t)(j0 + src);
+    });
 }
 
 // Warp-per-tile bitonic sort for bins of <= 1024 entries, in registers: element i = 32 e + lane

@@ -262,76 +262,58 @@ __global__ void __launch_bounds__(256) groups_kernel(void *tables, const float2 
     }
 }
 
-// K2d: the superposition kernel's window LUT (internal.h), re-grouped from the canonical lists.
-// One thread per pointer slot (depth, level, variant v, band k, column group xg): it visits the
-// canonical (band, Xb) ranges that cover rows [bs, bs + 32), bs = v q_l + 32 (k - 1), and columns
-// [xg G_l, (xg + 1) G_l), and counts (pass 0) or writes (pass 1) the entries whose row falls in
-// the band: value (float2) and position (Y - bs) S + X (uint16), in canonical order.
-__global__ void __launch_bounds__(256) vgroups_kernel(void *tables, int n_depth, int L, int T, int S, int pass) {
+// K2d: the superposition kernel's window LUT (internal.h), built per canonical entry: each kept entry
+// (level l, X, Y) of table d belongs, for every variant v of its level, to band k = (Y - v q_l) / 32 + 1
+// and column group X >> lg_l.  Pass 0 counts (atomics on the slot counters), pass 1 places it at a
+// slot cursor (atomics on a copy of the scanned pointers).  The order inside a group is then
+// arbitrary: a window range belongs to one point, whose targets are distinct, so every result is
+// bitwise the same whatever that order (R-A11 holds per pixel).  C4: 3e6 entries x ~11 variants.
+__global__ void __launch_bounds__(256) ventries_kernel(void *tables, int n_tab, int L, int S, int pass,
+                                                       int32_t *__restrict__ cursor) {
     const TableHeader &h = hdr(tables);
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= h.total_vptrs) return;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= h.total_entries) return;
     const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
     const KDesc *kd = at<KDesc>(tables, h.kdesc_off);
-    int32_t *vptr = atw<int32_t>(tables, h.vptr_off);
-    int lo = 0, hi = n_depth;
+    const int32_t *ptr = at<int32_t>(tables, h.ptr_off);
+    const uint4 en = at<uint4>(tables, h.ent_off)[e];
+    // table of entry e: largest d with ptr[group_base_d] <= e (canonical entries are in table order)
+    int lo = 0, hi = n_tab;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (dd[mid].vgroup_base <= g) lo = mid; else hi = mid;
+        if (ptr[dd[mid].group_base] <= e) lo = mid; else hi = mid;
     }
-    const int d = lo;
-    const KDesc K = kd[d];
-    const int side = dd[d].side;
-    int l = 1;
-    while (l < L && K.vptr_base[l] <= g) l++;
-    const int ncol = win_cols(side, l), nband = win_bands(side);
-    const int64_t local = g - K.vptr_base[l - 1];
-    const int xg = (int)(local % (ncol + 1));
-    if (xg == ncol) {  // dummy slot: band end
-        if (pass == 0) vptr[g] = 0;
-        return;
-    }
-    const int row = (int)(local / (ncol + 1));
-    const int v = row / nband, k = row % nband;
-    const int bs = (v << win_lq(l, h.cls_bits)) + kWinRows * (k - 1);
-    const int y0 = max(bs, 0), y1 = min(bs + kWinRows, side);
-    const int lg = win_lg(l);
-    const int nb = side >> l, bh = band_blocks(T, l) << l;              // canonical band height (px)
-    const int xb0 = (xg << lg) >> l, xb1 = min(((xg + 1) << lg) >> l, nb);  // canonical block columns
-    const int32_t *ptr = at<int32_t>(tables, h.ptr_off);
-    const uint4 *ent = at<uint4>(tables, h.ent_off);
+    const int d = lo, side = dd[d].side;
+    const int X = (int)(en.x & 0x3fffu), Y = (int)((en.x >> 14) & 0x3fffu), l = (int)(en.x >> 28);
+    const int lq = win_lq(l, h.cls_bits), nv = win_variants(l, h.cls_bits), nband = win_bands(side);
+    const int ncol = win_cols(side, l), xg = X >> win_lg(l);
+    int32_t *vptr = atw<int32_t>(tables, h.vptr_off);
     float2 *vval = atw<float2>(tables, h.vval_off);
     uint16_t *vpos = atw<uint16_t>(tables, h.vpos_off);
-    int out = pass ? vptr[g] : 0, cnt = 0;
-    if (y0 < y1) {
-        for (int cb = y0 / bh; cb <= (y1 - 1) / bh; cb++) {
-            const int crow = K.ptr_base[l - 1] + cb * (nb + 1);
-            const int e0 = ptr[crow + xb0], e1 = ptr[crow + xb1];
-            for (int e = e0; e < e1; e++) {
-                const uint4 en = ent[e];
-                const int Y = (int)((en.x >> 14) & 0x3fffu), X = (int)(en.x & 0x3fffu);
-                if (Y < bs || Y >= bs + kWinRows) continue;
-                if (pass) {
-                    vval[out] = make_float2(__uint_as_float(en.y), __uint_as_float(en.z));
-                    vpos[out] = (uint16_t)((Y - bs) * S + X);
-                    out++;
-                }
-                cnt++;
-            }
+    for (int v = 0; v < nv; v++) {
+        const int k = ((Y - (v << lq)) >> 5) + 1;            // floor division (arithmetic shift)
+        const int bs = (v << lq) + kWinRows * (k - 1);
+        const int64_t slot = kd[d].vptr_base[l - 1] + (int64_t)(v * nband + k) * (ncol + 1) + xg;
+        if (pass == 0) {
+            atomicAdd(&vptr[slot], 1);
+        } else {
+            const int out = atomicAdd(&cursor[slot], 1);
+            vval[out] = make_float2(__uint_as_float(en.y), __uint_as_float(en.z));
+            vpos[out] = (uint16_t)((Y - bs) * S + X);
         }
     }
-    if (pass == 0) vptr[g] = cnt;
 }
 
 }  // namespace
 
-cudaError_t launch_vgroups(const TableHeader &h, void *d_tables, int pass, cudaStream_t s) {
-    const unsigned blocks = (unsigned)((h.total_vptrs + 255) / 256);
+cudaError_t launch_ventries(const TableHeader &h, void *d_tables, int pass, int32_t *cursor, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((h.total_entries + 255) / 256);
     if (blocks == 0) return cudaSuccess;
     count_launches(1);
-    vgroups_kernel<<<blocks, 256, 0, s>>>(d_tables, h.n_depth, h.levels, h.tile, h.S, pass);
+    ventries_kernel<<<blocks, 256, 0, s>>>(d_tables, h.n_depth, h.levels, h.S, pass, cursor);
     return cudaGetLastError();
 }
+
 
 cudaError_t launch_psf_haar(const TableHeader &h, const void *d_tables, float2 *coef_val, uint32_t *coef_key,
                             double k, double pitch, int levels, int n_depth, cudaStream_t s) {

@@ -170,7 +170,7 @@ struct Geo {
     int64_t total_entries = 0, total_ptrs = 0, total_ctas = 0, total_coef = 0, max_E = 0, total_vptrs = 0;
     TableHeader th;
     size_t table_bytes = 0, scratch_bytes = 0;
-    size_t sc_val = 0, sc_key = 0, sc_hist = 0, sc_sel = 0, sc_scan = 0;
+    size_t sc_val = 0, sc_key = 0, sc_hist = 0, sc_sel = 0, sc_scan = 0, sc_cursor = 0;
 };
 
 double level_z(const wasabi_params &P, double dz, int d) {
@@ -281,6 +281,7 @@ wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
     g.sc_hist = so; so = align_up(so + 4 * 256 * (size_t)g.nd, 256);
     g.sc_sel = so; so = align_up(so + 24 * (size_t)g.nd, 256);
     g.sc_scan = so; so = align_up(so + scan_scratch_bytes(std::max(ptr, vptr) + 1), 256);
+    g.sc_cursor = so; so = align_up(so + 4 * (size_t)(vptr + 1), 256);   // window-LUT slot cursors
     if (g.wav) {   // fp64 work and ping-pong tables, per-level work-item prefixes
         g.pre.assign((size_t)g.L * (g.nd + 1), 0);
         for (int l = 1; l <= g.L; l++)
@@ -451,10 +452,13 @@ wasabi_status wasabi_build_psf_tables(const wasabi_params *params, void *d_table
     CK(launch_groups(g.th, d_tables, cval, ckey, sel, 1, stream), "groups scatter");
     // the superposition kernel's window LUT, re-grouped from the canonical lists
     CK(cudaMemsetAsync(tb + g.th.vptr_off, 0, 4 * (size_t)(g.total_vptrs + 1), stream), "memset vptr");
-    CK(launch_vgroups(g.th, d_tables, 0, stream), "vgroups count");
+    int32_t *cursor = reinterpret_cast<int32_t *>(sb + g.sc_cursor);
+    CK(launch_ventries(g.th, d_tables, 0, cursor, stream), "window LUT count");
     CK(launch_scan_i32(reinterpret_cast<int32_t *>(tb + g.th.vptr_off), g.total_vptrs + 1, sb + g.sc_scan, stream),
        "scan vptr");
-    CK(launch_vgroups(g.th, d_tables, 1, stream), "vgroups scatter");
+    CK(cudaMemcpyAsync(cursor, tb + g.th.vptr_off, 4 * (size_t)(g.total_vptrs + 1), cudaMemcpyDeviceToDevice, stream),
+       "window LUT cursors");
+    CK(launch_ventries(g.th, d_tables, 1, cursor, stream), "window LUT scatter");
     return WASABI_OK;
 }
 
