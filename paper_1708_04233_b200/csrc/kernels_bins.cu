@@ -79,7 +79,9 @@ __device__ __forceinline__ void warp_footprint(int4 q, bool valid, const KDesc *
         const int Q = __ldg(&kd[tb].Q);
         int tx0, tx1, ty0, ty1;
         tile_range(ix, iy, __ldg(&kd[tb].Ek), A, tx0, tx1, ty0, ty1);
-        const int w = tx1 - tx0 + 1, nbox = w * (ty1 - ty0 + 1);
+        const int w = tx1 - tx0 + 1, hgt = ty1 - ty0 + 1;
+        if (w <= 0 || hgt <= 0) continue;              // footprint entirely outside the band
+        const int nbox = w * hgt;
         for (int i = lane; i < nbox; i += 32) {
             const int ty = ty0 + i / w, tx = tx0 + i % w;
             const int rem = Q - sq_gap(iy, (int)A.row0 + ty * A.T, A.T);

@@ -87,3 +87,43 @@ class Pipeline:
             self.superpose()
             self.inverse()
         return self.field, self.bits
+
+
+class HologramStream:
+    """Band-by-band generation of a print pattern with buffers for one band only -- the paper's
+    sub-hologram division "to reduce the memory usage", so the hologram may be
+    far larger than device memory: the tables are built once, then each 2^L-aligned band of
+    `band_rows` rows is binned and run through the fused superpose/inverse/quantise kernel in
+    print-only mode, and its bits are copied to the host.  `run(points)` yields (row0, bits) with
+    bits a (rows, n_h // 8) uint8 numpy array; concatenated they equal the full hologram's bits
+    bit for bit (R-A11: bands are independent).  Haar mode only (coiflets need psi halos)."""
+
+    def __init__(self, p: Params, n_max: int, band_rows: int, device=None,
+                 print_params: Optional[PrintParams] = None, stream=None):
+        import torch
+        if p.wavelet != 0:
+            raise ValueError("HologramStream: the coiflet inverse needs psi halos; use Pipeline per band")
+        if band_rows % p.tile or band_rows <= 0:
+            raise ValueError("band_rows must be a positive multiple of the tile")
+        self.torch, self.p, self.band_rows, self.stream = torch, p, band_rows, stream
+        self.device = torch.device(device if device is not None else "cuda")
+        self.print_params = print_params if print_params is not None else PrintParams()
+        tb, sb = psf_tables_bytes(p)
+        self.tables = torch.empty(tb, dtype=torch.uint8, device=self.device)
+        self.scratch = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        self.bins = torch.empty(bin_points_bytes(p, n_max, 0, band_rows), dtype=torch.uint8, device=self.device)
+        self.bits = torch.empty((band_rows, p.n_h // 8), dtype=torch.uint8, device=self.device)
+        self.h_bits = torch.empty((band_rows, p.n_h // 8), dtype=torch.uint8).pin_memory()
+
+    def run(self, points):
+        torch = self.torch
+        build_psf_tables(self.p, self.tables, self.scratch, self.stream)
+        for row0 in range(0, self.p.n_h, self.band_rows):
+            row1 = min(self.p.n_h, row0 + self.band_rows)
+            rows = row1 - row0
+            bin_points(self.p, self.tables, points, row0, row1, self.bins, self.stream)
+            superpose_inverse(self.p, self.tables, self.bins, row0, row1, self.print_params, None,
+                              self.bits[:rows], self.stream)
+            self.h_bits[:rows].copy_(self.bits[:rows], non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize() if self.stream is None else self.stream.synchronize()
+            yield row0, self.h_bits[:rows].numpy().copy()

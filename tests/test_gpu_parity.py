@@ -409,3 +409,18 @@ def test_wasabi_keep_all_aligned_equals_gpu_direct_sum(W):
     _, _, u_w, _ = _gpu_run(W, cfg, pts, 0, 2048)
     _, u_d = _direct_gpu(W, cfg, pts, 0, 2048)
     assert rel_l2(u_w, u_d) <= 1e-5
+
+
+def test_hologram_stream_equals_full(W):
+    """Band-by-band streaming (PAPER.md:115-116 sub-holograms; buffers for one band only) gives the
+    full hologram's print bits bit for bit."""
+    import torch
+    cfg = CONFIGS["C2"]
+    pts = make_points(cfg, n=4000)
+    _, _, _, bits_full = _gpu_run(W, cfg, pts, 0, 2048)
+    p = gpu_params(cfg)
+    hs = W.pipeline.HologramStream(p, len(pts), 384)
+    d = torch.from_numpy(pts).cuda()
+    parts = list(hs.run(d))
+    assert [r for r, _ in parts] == list(range(0, 2048, 384))
+    assert np.array_equal(np.concatenate([b for _, b in parts]), bits_full)
