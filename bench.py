@@ -268,6 +268,13 @@ def run_ours(args, cfg):
             if isinstance(rec, dict):
                 traffic = rec.get("traffic")
                 onchip = rec.get("onchip")
+                prof_rows = rec.get("rows")
+                if traffic is not None and prof_rows and prof_rows != rows and cfg.name == "C4":
+                    # the capture is of the full hologram; a band moves its share of it
+                    traffic = traffic * rows / prof_rows
+                    onchip = dict(onchip or {}, traffic_scaled_from_rows=prof_rows)
+                elif cfg.name != "C4":
+                    traffic, onchip = None, None   # the capture is of C4 only
             else:
                 traffic = rec
         except Exception:
