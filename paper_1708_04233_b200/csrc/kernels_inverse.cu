@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(256) inverse_kernel(const float2 *psi, float2 
         *reinterpret_cast<float4 *>(&s[row * kS + 2 * c4]) = v;
     }
     __syncthreads();
-    inverse_haar_tile(s, kT, kS, L, threadIdx.x, 256);
+    inverse_haar_tile_blk4(s, kT, kS, L, threadIdx.x, 256);
     if (write_u) {
         float4 *dst = reinterpret_cast<float4 *>(u);
 #pragma unroll
