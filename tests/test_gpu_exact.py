@@ -90,3 +90,21 @@ def test_exact_rejects_deep_levels(W):
     p = gpu_params(cfg, exact=True)           # L = 5: 4^5 tables per depth -> refused
     with pytest.raises(W.WasabiError, match="EXACT_SHIFT"):
         W.psf_tables_bytes(p)
+
+
+def test_exact_hologram_host_equals_device_path(W):
+    """The whole path from host buffers (chunked superposition, side-stream copies) in the
+    offset-class mode equals the device pipeline bit for bit."""
+    import torch
+    cfg = CONFIGS["C1"]
+    pts = make_points(cfg)
+    p = gpu_params(cfg, exact=True)
+    _, _, u_g, bits_g = _gpu_run(W, cfg, pts, 128, 384, exact=True)
+    ws = torch.empty(W.hologram_workspace_bytes(p, len(pts), 128, 384), dtype=torch.uint8, device="cuda")
+    h_bits = torch.empty((256, p.n_h // 8), dtype=torch.uint8)
+    h_u = torch.empty((256, p.n_h, 2), dtype=torch.float32)
+    W.hologram_host(p, W.PrintParams(), torch.from_numpy(pts), 128, 384, ws, h_bits, h_u)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_bits.numpy(), bits_g)
+    hu = h_u.numpy()
+    assert np.array_equal(hu[..., 0] + 1j * hu[..., 1], u_g.astype(np.complex64).astype(np.complex128))
