@@ -57,4 +57,4 @@ for name, cl in [("v14 classes", cls), ("l1 | rest", {0: [1], 1: [2, 3, 4, 5, 6]
                 nz_ranges += (nl > 0).sum(); ch_rng += np.ceil(nl / 32).sum()
     print(f"{name}: chunks per-point-flattened {ch_pt:.3e}  per-range {ch_rng:.3e}  mixed {ch_mix:.3e}  "
           f"units {units:.3e} nonempty level-ranges {nz_ranges:.3e}")
-np.savez_compressed("/tmp/ranges_c4.npz", cnt=cnt)
+np.savez_compressed("/tmp/ranges_c4.npz", cnt=cnt, ptr=ptr)
