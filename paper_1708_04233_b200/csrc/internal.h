@@ -62,6 +62,8 @@ __host__ __device__ inline int win_variants(int l, int cb) { return kWinRows >> 
 __host__ __device__ inline int win_bands(int side) { return (side + kWinRows - 1) / kWinRows + 1; }
 __host__ __device__ inline int win_cols(int side, int l) { return (side + (1 << win_lg(l)) - 1) >> win_lg(l); }
 // pointer slots of level l of one table
+// window-LUT positions are uint16 (Y - band start) * S + X: 31 (T + margin) + side - 1 must fit
+static_assert(31 * (128 + kWinMargin) + kMaxTableSide - 1 <= 65535, "window-LUT positions overflow uint16");
 __host__ __device__ inline int win_slots(int side, int l, int cb) {
     return win_variants(l, cb) * win_bands(side) * (win_cols(side, l) + 1);
 }
