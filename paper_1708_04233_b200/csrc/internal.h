@@ -51,9 +51,13 @@ __host__ __device__ inline int table_of(int ix, int iy, int iz, int cb) {
 // which land in the shared tile's margin columns (never read).
 constexpr int kWinRows = 32;
 #ifndef WASABI_WIN_MARGIN
-#define WASABI_WIN_MARGIN 6
+#define WASABI_WIN_MARGIN 8
 #endif
-constexpr int kWinMargin = WASABI_WIN_MARGIN;   // >= 6 (level-1 column-group overrun)
+// >= 6 (level-1 column-group overrun); 8 so that the shared tile's rows (stride T + 8) start on
+// 8-cell (64-byte) boundaries and the superposition kernel's bank swizzle (an XOR of address
+// bits 3..5) keeps every margin cell inside a margin block
+constexpr int kWinMargin = WASABI_WIN_MARGIN;
+static_assert(kWinMargin >= 6 && kWinMargin % 8 == 0, "window margin: >= 6 and a multiple of 8");
 // log2 q_l: window starts are multiples of min(2^l, 32); with offset-class tables (cb = L class
 // bits, R-A20) every level is shifted by multiples of 2^L, so of min(2^max(l, L), 32)
 __host__ __device__ inline int win_lq(int l, int cb) { const int m = l > cb ? l : cb; return m < 5 ? m : 5; }

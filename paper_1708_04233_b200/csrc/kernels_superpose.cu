@@ -36,7 +36,7 @@ struct SupArgs {
 };
 
 #ifndef WASABI_KD
-#define WASABI_KD 8
+#define WASABI_KD 6
 #endif
 #ifndef WASABI_MINB
 #define WASABI_MINB 5
@@ -77,6 +77,25 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 }
 constexpr unsigned kFull = 0xffffffffu;
 
+#ifndef WASABI_SWZ
+#define WASABI_SWZ 1
+#endif
+// Shared-tile bank swizzle.  A level-l coefficient sits at a pixel whose X and Y are multiples of
+// 2^(l-1) (R-A6), so in a linear tile the cells of a level-2 chunk fall on even bank pairs and
+// those of a level-3 chunk on a quarter of them: ~6.2 wavefronts per 32-lane LDS.64 against an
+// ideal 2 (ncu, v19; tools/bank_model.py reproduces it).  The byte address a of a cell is replaced
+// by a ^ ((a >> 5) & 0x38): address bits 3..5 (the cell inside its 64-byte block) XOR address
+// bits 8..10, a permutation inside each aligned 8-cell block.  With rows of stride S = T + 8 cells
+// starting on 64-byte boundaries (tile base 64-byte aligned), margin blocks stay margin blocks; the
+// model predicts ~3.5 wavefronts per chunk.
+__device__ __forceinline__ uint32_t swz(uint32_t a) {
+#if WASABI_SWZ
+    return a ^ ((a >> 5) & 0x38u);
+#else
+    return a;
+#endif
+}
+
 __device__ __forceinline__ float2 lds2(uint32_t a) {
     float2 v;
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
@@ -99,7 +118,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
                                                                            int fused, QArgs qa,
                                                                            uint8_t *__restrict__ bits) {
     constexpr int M = kWinMargin, S = T + M, NT = 2 * T;
-    constexpr int kData = M + T * S + M;      // margin-padded tile; per-warp dummy cells follow
+    constexpr int kData = M + T * S + M;      // margin-padded tile; a block of per-warp dummy cells follows
+    static_assert(S % 8 == 0 && M % 8 == 0 && NT / 32 <= 8, "swizzle blocks");
     extern __shared__ float2 tile[];
     const char *bb = reinterpret_cast<const char *>(d_bins);
     const BinHeader *bh = reinterpret_cast<const BinHeader *>(bb);
@@ -122,8 +142,13 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     const int strip_base = M + kWinRows * strip * S;   // smem index of (strip row 0, column 0)
     const int dummy = kData + wid;
     const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(tile);
+    if (tile_sa & 63u) __trap();              // the swizzle permutes 64-byte blocks of the tile
+    // pixel (r, x) of the tile: cell M + r S + x, swizzled
+    auto cell = [&](int r, int x) -> float2 & {
+        return tile[(swz(tile_sa + 8u * (uint32_t)(M + r * S + x)) - tile_sa) >> 3];
+    };
 
-    for (int i = threadIdx.x; i < kData + NT / 32; i += NT) tile[i] = make_float2(0.f, 0.f);
+    for (int i = threadIdx.x; i < kData + 8; i += NT) tile[i] = make_float2(0.f, 0.f);
     __syncthreads();
 
     const int lv0 = class_level(cls, 0, A.L), lv1 = class_level(cls, 1, A.L);
@@ -268,7 +293,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     } while (0)
 #define WASABI_CONSUME(u)                                                           \
     do {                                                                            \
-        const uint32_t sa = rb[u] + 8u * (uint32_t)rp[u];                           \
+        const uint32_t sa = swz(rb[u] + 8u * (uint32_t)rp[u]);                      \
         float2 o = lds2(sa);                                                        \
         o.x = fmaf(ra[u], rv[u].x, o.x);                                            \
         o.y = fmaf(ra[u], rv[u].y, o.y);                                            \
@@ -300,10 +325,17 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 #undef WASABI_PREFETCH
 #undef WASABI_CONSUME
     __syncthreads();
-    float2 *data = tile + M;                    // row r, column x at data[r * S + x]
     if (fused) {
-        // steps 3 (+4) in place: psi never leaves shared memory
-        inverse_haar_tile(data, T, S, A.L, threadIdx.x, NT);
+        // steps 3 (+4) in place: psi never leaves shared memory; the
+        // butterflies of inverse_haar_tile (device_common.cuh) in the same order, swizzled cells
+        for (int l = A.L; l >= 1; l--) {
+            const int st = 1 << (l - 1), nq = T >> l;
+            for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
+                const int bx = (qd % nq) << l, by = (qd / nq) << l;
+                inv_butterfly(&cell(by, bx), &cell(by, bx + st), &cell(by + st, bx), &cell(by + st, bx + st));
+            }
+            __syncthreads();
+        }
         if (bits) {
             constexpr int bpr = T / 8;
             for (int bi = threadIdx.x; bi < T * bpr; bi += NT) {
@@ -313,7 +345,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
                     const int x = xb * 8 + i;
-                    const float I = interference(data[row * S + x], tile_x0 + x, Y, qa);
+                    const float I = interference(cell(row, x), tile_x0 + x, Y, qa);
                     byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
                 }
                 bits[(Y - A.row0) * (A.n_h / 8) + tile_x0 / 8 + xb] = (uint8_t)byte;
@@ -323,14 +355,14 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     }
     float2 *out = psi + (int64_t)(tile_y0 - A.row0) * A.n_h + tile_x0;
     for (int y = wid; y < T; y += NT / 32)
-        for (int x = lane; x < T; x += 32) out[(int64_t)y * A.n_h + x] = data[y * S + x];
+        for (int x = lane; x < T; x += 32) out[(int64_t)y * A.n_h + x] = cell(y, x);
 }
 
 template <int T, bool EX>
 cudaError_t launch_t(const void *d_bins, const void *d_tables, const SupArgs &A, int64_t n_tiles, float2 *psi,
                      int fused, const QArgs &qa, uint8_t *bits, cudaStream_t s) {
     constexpr int M = kWinMargin, S = T + M;
-    const int smem = (M + T * S + M + T / 16) * (int)sizeof(float2);
+    const int smem = (M + T * S + M + 8) * (int)sizeof(float2);
     cudaError_t e = cudaFuncSetAttribute(superpose_kernel<T, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (n_tiles > 0) {
