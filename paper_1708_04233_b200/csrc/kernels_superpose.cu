@@ -33,6 +33,7 @@ struct SupArgs {
     int L, cls_bits, tiles_x;
     int64_t row0, n_h;
     int64_t tile0;   // first tile (row-major in the bins' band) of this launch
+    int tile_rows;   // tile rows of this launch
 };
 
 #ifndef WASABI_KD
@@ -46,6 +47,15 @@ struct SupArgs {
 #endif
 
 constexpr int kD = WASABI_KD;          // register ring depth (chunks in flight per warp)
+
+#ifndef WASABI_GROUP
+#define WASABI_GROUP 32
+#endif
+// Tile order: groups of kGroup tile rows, column-major inside a group, so that the CTAs resident
+// at one time cover a compact 2-D region (kGroup x ~23 tiles at 740 resident CTAs) instead of a
+// full-width tile row: its points span fewer depth tables, and more of the window-LUT reads hit
+// L2 (0 = row-major).
+constexpr int kGroup = WASABI_GROUP;
 
 #ifndef WASABI_L1NA
 #define WASABI_L1NA 0
@@ -135,7 +145,15 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int cls = wid & 1, strip = wid >> 1;
-    const int64_t t = A.tile0 + blockIdx.x;
+    int64_t t;
+    if (kGroup > 0) {
+        const int64_t per_group = (int64_t)kGroup * A.tiles_x;
+        const int64_t g = blockIdx.x / per_group, rem = blockIdx.x - g * per_group;
+        const int gh = (int)min((int64_t)kGroup, A.tile_rows - g * kGroup);
+        t = A.tile0 + (g * kGroup + rem % gh) * A.tiles_x + rem / gh;
+    } else {
+        t = A.tile0 + blockIdx.x;
+    }
     const int tile_x0 = (int)(t % A.tiles_x) * T;
     const int tile_y0 = (int)(A.row0 + (t / A.tiles_x) * (int64_t)T);
     const int strip_y0 = tile_y0 + kWinRows * strip;
@@ -382,6 +400,7 @@ cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, in
     SupArgs A;
     A.L = L; A.cls_bits = cls_bits; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
     A.tile0 = (int64_t)tile_row0 * tiles_x;
+    A.tile_rows = tile_row1 - tile_row0;
     const int64_t n_tiles = (int64_t)tiles_x * (tile_row1 - tile_row0);
     const QArgs qa = make_qargs(print4, pitch, n_h);
     if (cls_bits)
