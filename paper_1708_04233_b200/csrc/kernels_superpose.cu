@@ -177,7 +177,6 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     // batch state: lane = point; per level slot j its range (beg, len) and smem base
     float a_l = 0.f;
     int beg[4], len[4], base[4];
-    unsigned msk[4];
     const int cb = EX ? A.L : 0;               // offset-class bits (R-A20) or 0
     const int cmask = (1 << cb) - 1;
     auto range = [&](int l, int ix, int iy, int H, int side, int vrow, bool ok, int &b, int &n, int &bs) {
@@ -202,16 +201,20 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         }
         bs = strip_base - xs;
     };
+    // the point records of the next batch are loaded one batch ahead and its bin indices two
+    // batches ahead (the loads overlap the ring): two dependent round trips off the batch phase
+    // (batches are 32 points but the last)
+    uint32_t nidx = pb + 32 + lane < b1 ? __ldg(bidx + pb + 32 + lane) : 0u;
+    int4 qn = pb + lane < b1 ? __ldg(pconv + __ldg(bidx + pb + lane)) : make_int4(0, 0, 0, 0);
     auto load_batch = [&]() -> bool {
         while (pb < b1) {
             const int nq = (int)min((unsigned long long)32, b1 - pb);
             const bool ok = lane < nq;
-            int4 q = make_int4(0, 0, 0, 0);
+            const int4 q = qn;
+            qn = pb + nq + lane < b1 ? __ldg(pconv + nidx) : make_int4(0, 0, 0, 0);
+            nidx = pb + nq + 32 + lane < b1 ? __ldg(bidx + pb + nq + 32 + lane) : 0u;
             int2 hv = make_int2(0, 0);          // (H, first window-LUT pointer slot)
-            if (ok) {
-                q = __ldg(pconv + __ldg(bidx + pb + lane));
-                hv = __ldg(reinterpret_cast<const int2 *>(&kd[table_of(q.x, q.y, q.z, cb)].H));
-            }
+            if (ok) hv = __ldg(reinterpret_cast<const int2 *>(&kd[table_of(q.x, q.y, q.z, cb)].H));
             pb += nq;
             a_l = __int_as_float(q.w);
             const int side = 2 * hv.x + (EX ? 1 << A.L : 0);
@@ -233,8 +236,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             bool any = false;
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-                msk[j] = __ballot_sync(kFull, len[j] > 0);
-                any |= msk[j] != 0u;
+                any |= __any_sync(kFull, len[j] > 0);
                 if (WASABI_PF && len[j] > 0) {
                     const int e0 = beg[j] & ~1, e1 = (beg[j] + len[j] + 1) & ~1;   // 16-byte granules
                     prefetch_l2(vval + e0, 8u * (uint32_t)(e1 - e0));
@@ -255,10 +257,10 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     bool have = false;
     int s_beg = 0, s_len = 0, s_base = 0;   // this lane's range for slot gj
     auto select_slot = [&]() {
-        gm = gj == 0 ? msk[0] : gj == 1 ? msk[1] : gj == 2 ? msk[2] : msk[3];
         s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : gj == 2 ? beg[2] : beg[3];
         s_len = gj == 0 ? len[0] : gj == 1 ? len[1] : gj == 2 ? len[2] : len[3];
         s_base = gj == 0 ? base[0] : gj == 1 ? base[1] : gj == 2 ? base[2] : base[3];
+        gm = __ballot_sync(kFull, s_len > 0);
     };
     auto next_range = [&]() {
         while (gm == 0u) {
@@ -372,8 +374,14 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         if (!psi) return;
     }
     float2 *out = psi + (int64_t)(tile_y0 - A.row0) * A.n_h + tile_x0;
-    for (int y = wid; y < T; y += NT / 32)
-        for (int x = lane; x < T; x += 32) out[(int64_t)y * A.n_h + x] = cell(y, x);
+#pragma unroll 4
+    for (int y = wid; y < T; y += NT / 32) {
+        float2 v[T / 32];                     // loads of a row first, then its coalesced stores
+#pragma unroll
+        for (int i = 0; i < T / 32; i++) v[i] = cell(y, lane + 32 * i);
+#pragma unroll
+        for (int i = 0; i < T / 32; i++) out[(int64_t)y * A.n_h + lane + 32 * i] = v[i];
+    }
 }
 
 template <int T, bool EX>
