@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         while (gm == 0u) {
             if (++gj >= 4) {         // batch exhausted: the outer loop loads the next one
                 have = false;
+                c_beg = c_end = 0;    // an empty range: the remaining ring slots idle
                 return;
             }
             select_slot();
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 #define WASABI_PREFETCH(u)                                                          \
     do {                                                                            \
         const int e = c_beg + lane;                                                 \
-        const bool v = have && e < c_end;                                           \
+        const bool v = e < c_end;                                                   \
         rp[u] = 0;                                                                  \
         if (v) {                                                                    \
             rv[u] = ldg_stream(vval + e);                                           \
@@ -306,10 +307,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         }                                                                           \
         rb[u] = v ? c_sa : dummy_sa;                                                \
         ra[u] = c_a;                                                                \
-        if (have) {                                                                 \
-            c_beg += 32;                                                            \
-            if (c_beg >= c_end) next_range();                                       \
-        }                                                                           \
+        c_beg += 32;                                                                \
+        if (c_beg >= c_end) next_range();                                           \
     } while (0)
 #define WASABI_CONSUME(u)                                                           \
     do {                                                                            \
