@@ -37,7 +37,7 @@ struct SupArgs {
 };
 
 #ifndef WASABI_KD
-#define WASABI_KD 6
+#define WASABI_KD 5
 #endif
 #ifndef WASABI_MINB
 #define WASABI_MINB 5
