@@ -21,6 +21,8 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tile", type=int, default=None)
 ap.add_argument("--fused", action="store_true", help="time superpose_inverse (fused path, as bench.py)")
 ap.add_argument("--pkg", default=None)
+ap.add_argument("--no-u", action="store_true", help="fused: bits only (no u write)")
+ap.add_argument("--no-bits", action="store_true", help="fused: u only (no binarisation)")
 ap.add_argument("--dump", default=None, help="np.save psi (after the timed superposes) to this path")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
@@ -28,7 +30,7 @@ if a.tile:
     cfg = cfg.replace(tile=a.tile)
 p = W.Params.from_config(cfg)
 pts = make_points(cfg)
-pl = W.Pipeline(p, len(pts), a.row0, a.row0 + a.rows)
+pl = W.Pipeline(p, len(pts), a.row0, a.row0 + a.rows, want_u=not a.no_u, want_bits=not a.no_bits)
 d = torch.from_numpy(pts).cuda()
 pl.run(d)
 torch.cuda.synchronize()
@@ -42,7 +44,7 @@ for _ in range(a.reps):
 ev[1].record()
 torch.cuda.synchronize()
 st = W.bins_stats(pl.bins)
-print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} {'fused' if a.fused else 'superpose'} {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
+print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} {('fused' + (' no-u' if a.no_u else '') + (' no-bits' if a.no_bits else '')) if a.fused else 'superpose'} {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
 if a.dump:
     import hashlib
     import numpy as np
