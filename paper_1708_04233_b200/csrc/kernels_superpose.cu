@@ -116,6 +116,9 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 }
 
 // levels of class c, slot j (0 = none): c = 0 -> {1, 3}, c = 1 -> {2, 4, 5, 6}
+#ifndef WASABI_STCS
+#define WASABI_STCS 1
+#endif
 #ifndef WASABI_CLS
 #define WASABI_CLS 1
 #endif
@@ -386,7 +389,13 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 #pragma unroll
         for (int i = 0; i < T / 32; i++) v[i] = cell(y, lane + 32 * i);
 #pragma unroll
-        for (int i = 0; i < T / 32; i++) out[(int64_t)y * A.n_h + lane + 32 * i] = v[i];
+        for (int i = 0; i < T / 32; i++) {
+#if WASABI_STCS   // write-once output: evict-first in L2, so it does not displace the window LUT
+            __stcs(out + (int64_t)y * A.n_h + lane + 32 * i, v[i]);
+#else
+            out[(int64_t)y * A.n_h + lane + 32 * i] = v[i];
+#endif
+        }
     }
 }
 
