@@ -5,7 +5,7 @@
 //
 // Design (DESIGN.md §6 "Superpose").  One CTA owns one T x T tile of psi in shared memory and
 // walks the tile's bin (points in ascending order).  Warp w owns the pixels of level class
-// c = w & 1 ({1, 3} or {2, 4, 5, 6}; every Haar level occupies its own pixels) in the 32-row strip
+// c = w & 1 ({1, 3, 6} or {2, 4, 5}; every Haar level occupies its own pixels) in the 32-row strip
 // w >> 1, so the warps of a CTA accumulate concurrently without atomics.  For a point and a level
 // of its class, the kept coefficients landing in the strip are ONE contiguous range of the window
 // LUT (internal.h: per-variant 32-row bands, column-group pointers), so a batch of 32 points
@@ -37,7 +37,7 @@ struct SupArgs {
 };
 
 #ifndef WASABI_KD
-#define WASABI_KD 5
+#define WASABI_KD 6
 #endif
 #ifndef WASABI_MINB
 #define WASABI_MINB 5
@@ -115,15 +115,17 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
 
-// levels of class c, slot j (0 = none): c = 0 -> {1, 3}, c = 1 -> {2, 4, 5, 6}
+// levels of class c, slot j (0 = none): c = 0 -> {1, 3, 6}, c = 1 -> {2, 4, 5}
 #ifndef WASABI_STCS
 #define WASABI_STCS 1
 #endif
 #ifndef WASABI_CLS
-#define WASABI_CLS 1
+#define WASABI_CLS 2
 #endif
 __device__ __forceinline__ int class_level(int c, int j, int L) {
-#if WASABI_CLS == 1   // {1, 3} / {2, 4, 5, 6}: 0.3% faster at C4 than {1, 4, 5, 6} / {2, 3}
+#if WASABI_CLS == 2   // {1, 3, 6} / {2, 4, 5}: three level slots per warp
+    const int l = c == 0 ? (j == 0 ? 1 : j == 1 ? 3 : j == 2 ? 6 : 0) : (j == 0 ? 2 : j < 3 ? j + 3 : 0);
+#elif WASABI_CLS == 1   // {1, 3} / {2, 4, 5, 6}: 0.3% faster at C4 than {1, 4, 5, 6} / {2, 3}
     const int l = c == 0 ? (j < 2 ? 2 * j + 1 : 0) : (j == 0 ? 2 : j + 3);
 #else
     const int l = c == 0 ? (j == 0 ? 1 : j + 3) : (j < 2 ? j + 2 : 0);
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 
     // batch state: lane = point; per level slot j its range (beg, len) and smem base
     float a_l = 0.f;
+    constexpr int kSlots = WASABI_CLS == 2 ? 3 : 4;   // level slots per warp
     int beg[4], len[4], base[4];
     const int cb = EX ? A.L : 0;               // offset-class bits (R-A20) or 0
     const int cmask = (1 << cb) - 1;
@@ -242,10 +245,10 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             range(lv0, q.x, q.y, hv.x, side, vr[0], ok, beg[0], len[0], base[0]);
             range(lv1, q.x, q.y, hv.x, side, vr[1], ok, beg[1], len[1], base[1]);
             range(lv2, q.x, q.y, hv.x, side, vr[2], ok, beg[2], len[2], base[2]);
-            range(lv3, q.x, q.y, hv.x, side, vr[3], ok, beg[3], len[3], base[3]);
+            if (kSlots > 3) range(lv3, q.x, q.y, hv.x, side, vr[3], ok, beg[3], len[3], base[3]);
             bool any = false;
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
+            for (int j = 0; j < kSlots; j++) {
                 any |= __any_sync(kFull, len[j] > 0);
                 if (WASABI_PF && len[j] > 0) {
                     const int e0 = beg[j] & ~1, e1 = (beg[j] + len[j] + 1) & ~1;   // 16-byte granules
@@ -267,14 +270,14 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     bool have = false;
     int s_beg = 0, s_len = 0, s_base = 0;   // this lane's range for slot gj
     auto select_slot = [&]() {
-        s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : gj == 2 ? beg[2] : beg[3];
-        s_len = gj == 0 ? len[0] : gj == 1 ? len[1] : gj == 2 ? len[2] : len[3];
-        s_base = gj == 0 ? base[0] : gj == 1 ? base[1] : gj == 2 ? base[2] : base[3];
+        s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : (kSlots == 3 || gj == 2) ? beg[2] : beg[3];
+        s_len = gj == 0 ? len[0] : gj == 1 ? len[1] : (kSlots == 3 || gj == 2) ? len[2] : len[3];
+        s_base = gj == 0 ? base[0] : gj == 1 ? base[1] : (kSlots == 3 || gj == 2) ? base[2] : base[3];
         gm = __ballot_sync(kFull, s_len > 0);
     };
     auto next_range = [&]() {
         while (gm == 0u) {
-            if (++gj >= 4) {         // batch exhausted: the outer loop loads the next one
+            if (++gj >= kSlots) {    // batch exhausted: the outer loop loads the next one
                 have = false;
                 c_beg = c_end = 0;    // an empty range: the remaining ring slots idle
                 return;
