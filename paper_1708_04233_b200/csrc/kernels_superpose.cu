@@ -263,17 +263,18 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     };
 
     // range generator (warp-uniform): level slot gj, remaining points gm, current range
-    int gj = 0, c_beg = 0, c_end = 0, c_dpos = dummy;    // (c_sa, c_dpos) address the dummy cell
+    int gj = 0, c_beg = 0, c_end = 0;
     uint32_t c_sa = tile_sa;
     unsigned gm = 0u;
     float c_a = 0.f;
     bool have = false;
-    int s_beg = 0, s_len = 0, s_base = 0;   // this lane's range for slot gj
+    int s_beg = 0, s_pk = 0;                 // this lane's range for slot gj: first entry, (base << 16) | length
     auto select_slot = [&]() {
         s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : (kSlots == 3 || gj == 2) ? beg[2] : beg[3];
-        s_len = gj == 0 ? len[0] : gj == 1 ? len[1] : (kSlots == 3 || gj == 2) ? len[2] : len[3];
-        s_base = gj == 0 ? base[0] : gj == 1 ? base[1] : (kSlots == 3 || gj == 2) ? base[2] : base[3];
-        gm = __ballot_sync(kFull, s_len > 0);
+        const int sl = gj == 0 ? len[0] : gj == 1 ? len[1] : (kSlots == 3 || gj == 2) ? len[2] : len[3];
+        const int sb = gj == 0 ? base[0] : gj == 1 ? base[1] : (kSlots == 3 || gj == 2) ? base[2] : base[3];
+        s_pk = (int)(((uint32_t)sb << 16) | (uint32_t)sl);   // |base| < 2^15, length < 2^16
+        gm = __ballot_sync(kFull, sl > 0);
     };
     auto next_range = [&]() {
         while (gm == 0u) {
@@ -287,10 +288,9 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         const int p = __ffs(gm) - 1;
         gm &= gm - 1u;
         c_beg = __shfl_sync(kFull, s_beg, p);
-        c_end = c_beg + __shfl_sync(kFull, s_len, p);
-        const int bse = __shfl_sync(kFull, s_base, p);
-        c_sa = tile_sa + 8u * (uint32_t)bse;
-        c_dpos = dummy - bse;                 // position that maps an idle lane to its dummy cell
+        const int pk = __shfl_sync(kFull, s_pk, p);   // 3 shuffles per range: they use the L1TEX data pipe
+        c_end = c_beg + (pk & 0xffff);
+        c_sa = tile_sa + 8u * (uint32_t)(pk >> 16);
         c_a = __shfl_sync(kFull, a_l, p);
         have = true;
     };
