@@ -17,9 +17,11 @@
 // and independent of the band split (R-A11).  A kD-deep register ring keeps the loads of the next
 // chunks in flight across range and level boundaries of a batch (idle lanes address the warp's
 // dummy cell).  Column overrun of the level-1/2 column groups lands in kWinMargin
-// margin columns of the shared tile (never read).  The kernel is bound by the L1TEX/LSU data pipe
-// (scattered 8-byte shared-memory read-modify-writes with random bank conflicts + the LUT loads;
-// DESIGN.md §6).
+// margin columns of the shared tile (never read).  Shared accesses go through an XOR bank swizzle
+// (swz below), tiles run in groups of 32 tile rows (L2 reuse of the window LUT), and the next
+// batch's point records are prefetched during the ring.  The kernel sits between the L1TEX/LSU data
+// pipe (~80%: scattered 8-byte shared-memory read-modify-writes, LUT and pointer loads, shuffles)
+// and instruction issue / load latency.
 #include <cuda_runtime.h>
 #include <cstdint>
 
