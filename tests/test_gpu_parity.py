@@ -424,3 +424,27 @@ def test_hologram_stream_equals_full(W):
     parts = list(hs.run(d))
     assert [r for r, _ in parts] == list(range(0, 2048, 384))
     assert np.array_equal(np.concatenate([b for _, b in parts]), bits_full)
+
+
+def test_cuda_graph_replay_equals_eager(W):
+    """A whole step (tables, bins, fused superpose/inverse/quantise) captured in a CUDA graph: the
+    replay reads the points in place and reproduces the eager step bit for bit, also after new
+    point data is copied into the captured tensor."""
+    import torch
+    cfg = CONFIGS["C1"]
+    p = gpu_params(cfg)
+    pts_a = make_points(cfg)
+    pts_b = make_points(cfg, seed=cfg.seed + 1)
+    d = torch.from_numpy(pts_a).cuda()
+    pl = W.Pipeline(p, len(pts_a), 0, p.n_h)
+    pl.capture(d)
+    eager = W.Pipeline(p, len(pts_a), 0, p.n_h)
+    for pts in (pts_a, pts_b):
+        d.copy_(torch.from_numpy(np.ascontiguousarray(pts)))
+        pl.field.zero_()
+        pl.bits.zero_()
+        pl.replay()
+        eager.run(torch.from_numpy(np.ascontiguousarray(pts)).cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(pl.bits, eager.bits)
+        assert torch.equal(pl.field, eager.field)
