@@ -50,13 +50,10 @@ __global__ void __launch_bounds__(256) inverse_kernel(const float2 *psi, float2 
         for (int bi = threadIdx.x; bi < kT * 8; bi += 256) {
             const int row = bi >> 3, xb = bi & 7;
             const int64_t Y = row0 + Yl0 + row;
-            unsigned byte = 0;
+            float2 v[8];
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const int x = xb * 8 + i;
-                const float I = interference(s[row * kS + x], X0 + x, Y, q);
-                byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
-            }
+            for (int i = 0; i < 8; i++) v[i] = s[row * kS + xb * 8 + i];
+            const unsigned byte = print_byte(v, X0 + xb * 8, ref_row(Y, q), q);
             bits[(Yl0 + row) * (n_h / 8) + X0 / 8 + xb] = (uint8_t)byte;
         }
     }
@@ -75,13 +72,7 @@ __global__ void __launch_bounds__(256) quantize_kernel(const float2 *__restrict_
             v[2 * i] = make_float2(f.x, f.y);
             v[2 * i + 1] = make_float2(f.z, f.w);
         }
-        unsigned byte = 0;
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const float I = interference(v[i], xb * 8 + i, row0 + yl, q);
-            byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
-        }
-        bits[b] = (uint8_t)byte;
+        bits[b] = (uint8_t)print_byte(v, xb * 8, ref_row(row0 + yl, q), q);
     }
 }
 

@@ -375,13 +375,10 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             for (int bi = threadIdx.x; bi < T * bpr; bi += NT) {
                 const int row = bi / bpr, xb = bi % bpr;
                 const int64_t Y = tile_y0 + row;
-                unsigned byte = 0;
+                float2 v[8];
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    const int x = xb * 8 + i;
-                    const float I = interference(cell(row, x), tile_x0 + x, Y, qa);
-                    byte |= (I >= 0.0f ? 1u : 0u) << (7 - i);
-                }
+                for (int i = 0; i < 8; i++) v[i] = cell(row, xb * 8 + i);
+                const unsigned byte = print_byte(v, tile_x0 + xb * 8, ref_row(Y, qa), qa);
                 bits[(Y - A.row0) * (A.n_h / 8) + tile_x0 / 8 + xb] = (uint8_t)byte;
             }
         }
