@@ -224,10 +224,14 @@ def test_inverse_standalone(W, orc, L):
     assert rel_l2(field_np(u), u_o) <= 1e-6
 
 
-def test_quantize_standalone_same_input(W, orc):
+@pytest.mark.parametrize("ref", [REF, (0.0002, -0.0001, -0.002), (0.0, 0.0, -0.05)])
+def test_quantize_standalone_same_input(W, orc, ref):
     """Step 4 alone on the same u: bits identical except |I| <= 1e-6 rms(I) (the decision is taken
-    on identical inputs; only the fp64 phase reduction / fp32 sincos differ)."""
+    on identical inputs; only the fp64 phase reduction / fp32 (cos, sin) differ).  The references:
+    the paper's (series path of print_byte), one 2 mm from the hologram (every pixel takes its own
+    square root) and one between."""
     import torch
+    REF = ref
     cfg = CONFIGS["C2"]
     p = gpu_params(cfg)
     rng = np.random.default_rng(5)
