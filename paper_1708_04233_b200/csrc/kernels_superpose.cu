@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     __syncthreads();
     if (fused) {
         // steps 3 (+4) in place: psi never leaves shared memory; the
-        // butterflies of inverse_haar_tile (device_common.cuh) in the same order, swizzled cells
+        // R-A6 butterflies level by level from L (inv_butterfly, device_common.cuh), swizzled cells
         for (int l = A.L; l >= 1; l--) {
             const int st = 1 << (l - 1), nq = T >> l;
             for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
