@@ -5,6 +5,8 @@ table modes where valid (Haar R-A8, exact shifts R-A20, coif1 R-A21), through th
 the fp64 oracle: bins bit-exact, psi and u within 1e-5 rel L2, print bits identical outside the
 threshold band (R-A16).  The window LUT (variants, bands, column groups) and the shared-tile
 margins see table sides that are not multiples of 32 or 64, odd level counts and both tile sizes."""
+import os
+
 import numpy as np
 import pytest
 
@@ -44,7 +46,8 @@ def _case(seed):
     return P, tile, pts, rng
 
 
-@pytest.mark.parametrize("seed", range(12))
+# WASABI_RANDOM_SEEDS=<n> widens the sweep (the default run keeps 12 seeds per mode)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("WASABI_RANDOM_SEEDS", "12"))))
 @pytest.mark.parametrize("mode", ["haar", "exact", "coif"])
 def test_random_problem_parity(W, orc, seed, mode):
     import torch
