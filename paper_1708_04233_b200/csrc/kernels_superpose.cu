@@ -118,6 +118,9 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 }
 
 // levels of class c, slot j (0 = none): c = 0 -> {1, 3, 6}, c = 1 -> {2, 4, 5}
+#ifndef WASABI_DEBUG_BOUNDS
+#define WASABI_DEBUG_BOUNDS 0   // 1: trap on a shared access outside the tile or a LUT index outside the arrays
+#endif
 #ifndef WASABI_STCS
 #define WASABI_STCS 1
 #endif
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     do {                                                                            \
         const int e = c_beg + lane;                                                 \
         const bool v = e < c_end;                                                   \
+        if (WASABI_DEBUG_BOUNDS && v && (e < 0 || (int64_t)e >= th->vent_cap + 32)) __trap();   \
         rp[u] = 0;                                                                  \
         if (v) {                                                                    \
             rv[u] = ldg_stream(vval + e);                                           \
@@ -325,9 +329,15 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         c_beg += 32;                                                                \
         if (c_beg >= c_end) next_range();                                           \
     } while (0)
+#if WASABI_DEBUG_BOUNDS   // every shared access inside the CTA's tile + dummy block
+#define WASABI_CHECK_SA(sa) do { if ((sa) - tile_sa >= 8u * (uint32_t)(kData + 8)) __trap(); } while (0)
+#else
+#define WASABI_CHECK_SA(sa) do { } while (0)
+#endif
 #define WASABI_CONSUME(u)                                                           \
     do {                                                                            \
         const uint32_t sa = swz(rb[u] + 8u * (uint32_t)rp[u]);                      \
+        WASABI_CHECK_SA(sa);                                                        \
         float2 o = lds2(sa);                                                        \
         o.x = fmaf(ra[u], rv[u].x, o.x);                                            \
         o.y = fmaf(ra[u], rv[u].y, o.y);                                            \
