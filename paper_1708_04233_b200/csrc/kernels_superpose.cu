@@ -121,6 +121,12 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 #ifndef WASABI_DEBUG_BOUNDS
 #define WASABI_DEBUG_BOUNDS 0   // 1: trap on a shared access outside the tile or a LUT index outside the arrays
 #endif
+#ifndef WASABI_BULKZERO
+#define WASABI_BULKZERO 1
+#endif
+#if WASABI_BULKZERO
+__device__ float4 g_zero[128 * (128 + kWinMargin + 2) / 2 + 16];   // zeros (static storage) for the tile fill
+#endif
 #ifndef WASABI_STCS
 #define WASABI_STCS 1
 #endif
@@ -183,8 +189,29 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         return tile[(swz(tile_sa + 8u * (uint32_t)(M + r * S + x)) - tile_sa) >> 3];
     };
 
+#if WASABI_BULKZERO
+    // zero the tile + dummy block by one bulk async copy from a zero buffer (the copy engine, not the
+    // LSU); the mbarrier sits after the dummy block
+    {
+        const uint32_t mbar = tile_sa + 8u * (uint32_t)(kData + 8);
+        constexpr uint32_t zbytes = 8u * (uint32_t)(kData + 8);
+        static_assert(zbytes % 16 == 0 && zbytes <= sizeof(g_zero), "bulk zero fill");
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(zbytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(tile_sa), "l"(g_zero), "r"(zbytes), "r"(mbar) : "memory");
+        }
+        __syncthreads();
+        asm volatile("{\n .reg .pred p;\n WZ_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+                     " @!p bra WZ_%=;\n}" ::"r"(mbar) : "memory");
+    }
+#else
     for (int i = threadIdx.x; i < kData + 8; i += NT) tile[i] = make_float2(0.f, 0.f);
     __syncthreads();
+#endif
 
     const int lv0 = class_level(cls, 0, A.L), lv1 = class_level(cls, 1, A.L);
     const int lv2 = class_level(cls, 2, A.L), lv3 = class_level(cls, 3, A.L);
@@ -415,7 +442,7 @@ template <int T, bool EX>
 cudaError_t launch_t(const void *d_bins, const void *d_tables, const SupArgs &A, int64_t n_tiles, float2 *psi,
                      int fused, const QArgs &qa, uint8_t *bits, cudaStream_t s) {
     constexpr int M = kWinMargin, S = T + M;
-    const int smem = (M + T * S + M + 8) * (int)sizeof(float2);
+    const int smem = (M + T * S + M + 8 + (WASABI_BULKZERO ? 1 : 0)) * (int)sizeof(float2);
     cudaError_t e = cudaFuncSetAttribute(superpose_kernel<T, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (n_tiles > 0) {
