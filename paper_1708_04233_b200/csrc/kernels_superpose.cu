@@ -18,7 +18,7 @@
 // chunks in flight across range and level boundaries of a batch (idle lanes address the warp's
 // dummy cell).  Column overrun of the level-1/2 column groups lands in kWinMargin
 // margin columns of the shared tile (never read).  Shared accesses go through an XOR bank swizzle
-// (swz below), tiles run in groups of 32 tile rows (L2 reuse of the window LUT), and the next
+// (swz below), tiles run in groups of 28 tile rows (L2 reuse of the window LUT), and the next
 // batch's point records are prefetched during the ring.  The kernel sits between the L1TEX/LSU data
 // pipe (~80%: scattered 8-byte shared-memory read-modify-writes, LUT and pointer loads, shuffles)
 // and instruction issue / load latency.
@@ -51,10 +51,10 @@ struct SupArgs {
 constexpr int kD = WASABI_KD;          // register ring depth (chunks in flight per warp)
 
 #ifndef WASABI_GROUP
-#define WASABI_GROUP 32
+#define WASABI_GROUP 28
 #endif
 // Tile order: groups of kGroup tile rows, column-major inside a group, so that the CTAs resident
-// at one time cover a compact 2-D region (kGroup x ~23 tiles at 740 resident CTAs) instead of a
+// at one time cover a compact, about square 2-D region (28 x ~26 tiles at 740 resident CTAs) instead of a
 // full-width tile row: its points span fewer depth tables, and more of the window-LUT reads hit
 // L2 (0 = row-major).
 constexpr int kGroup = WASABI_GROUP;
