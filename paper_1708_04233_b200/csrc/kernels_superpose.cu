@@ -102,7 +102,10 @@ constexpr unsigned kFull = 0xffffffffu;
 // model predicts ~3.5 wavefronts per chunk.
 __device__ __forceinline__ uint32_t swz(uint32_t a) {
 #if WASABI_SWZ
-    return a ^ ((a >> 5) & 0x38u);
+#ifndef WASABI_SWZ_SHIFT
+#define WASABI_SWZ_SHIFT 5
+#endif
+    return a ^ ((a >> WASABI_SWZ_SHIFT) & 0x38u);
 #else
     return a;
 #endif
