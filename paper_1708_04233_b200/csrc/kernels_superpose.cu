@@ -111,6 +111,14 @@ __device__ __forceinline__ uint32_t swz(uint32_t a) {
 #endif
 }
 
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
 __device__ __forceinline__ float2 lds2(uint32_t a) {
     float2 v;
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
@@ -129,6 +137,9 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
 #endif
 #if WASABI_BULKZERO
 __device__ float4 g_zero[128 * (128 + kWinMargin + 2) / 2 + 16];   // zeros (static storage) for the tile fill
+#endif
+#ifndef WASABI_L1Q
+#define WASABI_L1Q 1
 #endif
 #ifndef WASABI_STCS
 #define WASABI_STCS 1
@@ -404,6 +415,28 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         // R-A6 butterflies level by level from L (inv_butterfly, device_common.cuh), swizzled cells
         for (int l = A.L; l >= 1; l--) {
             const int st = 1 << (l - 1), nq = T >> l;
+#if WASABI_L1Q
+            if (l == 1) {   // a level-1 quad's rows are aligned 16-byte cell pairs (swapped for odd keys)
+                for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
+                    const int bx = (qd % nq) << 1, by = (qd / nq) << 1;
+                    const uint32_t a0 = swz(tile_sa + 8u * (uint32_t)(M + by * S + bx));
+                    const uint32_t a1 = swz(tile_sa + 8u * (uint32_t)(M + (by + 1) * S + bx));
+                    const float4 w0 = lds4(a0 & ~15u), w1 = lds4(a1 & ~15u);
+                    float2 q[4];
+                    q[0] = (a0 & 8u) ? make_float2(w0.z, w0.w) : make_float2(w0.x, w0.y);
+                    q[1] = (a0 & 8u) ? make_float2(w0.x, w0.y) : make_float2(w0.z, w0.w);
+                    q[2] = (a1 & 8u) ? make_float2(w1.z, w1.w) : make_float2(w1.x, w1.y);
+                    q[3] = (a1 & 8u) ? make_float2(w1.x, w1.y) : make_float2(w1.z, w1.w);
+                    inv_butterfly(&q[0], &q[1], &q[2], &q[3]);
+                    sts4(a0 & ~15u, (a0 & 8u) ? make_float4(q[1].x, q[1].y, q[0].x, q[0].y)
+                                              : make_float4(q[0].x, q[0].y, q[1].x, q[1].y));
+                    sts4(a1 & ~15u, (a1 & 8u) ? make_float4(q[3].x, q[3].y, q[2].x, q[2].y)
+                                              : make_float4(q[2].x, q[2].y, q[3].x, q[3].y));
+                }
+                __syncthreads();
+                continue;
+            }
+#endif
             for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
                 const int bx = (qd % nq) << l, by = (qd / nq) << l;
                 inv_butterfly(&cell(by, bx), &cell(by, bx + st), &cell(by + st, bx), &cell(by + st, bx + st));
