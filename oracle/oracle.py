@@ -125,6 +125,8 @@ def lib():
             L.orc_direct_d1.argtypes = [_pp, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                         _dp]
             L.orc_direct_d2.argtypes = L.orc_direct_d1.argtypes
+            L.orc_level_shift.argtypes = [_pp, C.c_int64, C.c_int]
+            L.orc_level_shift.restype = C.c_int64
             _lib = L
     return _lib
 
@@ -342,6 +344,11 @@ def quantize(P: Params, ref, u: np.ndarray, x0: int, y0: int):
     lib().orc_quantize(C.byref(P.c()), float(ref[0]), float(ref[1]), float(ref[2]), _ptr(b, _dp), x0, y0,
                        w, h, _ptr(bits, _u8p), _ptr(I, _dp))
     return bits, I
+
+
+def level_shift(P: Params, i: int, l: int) -> int:
+    """The oracle's level-l coefficient shift s_l(i) of pixel index i (R-A8; R-A20 in exact mode)."""
+    return int(lib().orc_level_shift(C.byref(P.c()), int(i), int(l)))
 
 
 def direct_d1(P: Params, pts, x0: int, y0: int, w: int, h: int) -> np.ndarray:

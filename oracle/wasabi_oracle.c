@@ -533,6 +533,10 @@ static int64_t orc_shift(const orc_params *P, int64_t i, int l) {
     return b * q;
 }
 
+/* Exported for the R-A8 pins (tests/test_oracle_shift.py): the level-l coefficient shift of
+ * pixel index i (orc_shift). */
+int64_t orc_level_shift(const orc_params *P, int64_t i, int l) { return orc_shift(P, i, l); }
+
 /* Reach of table d's kept list (reading R-A19; exact mode R-A20: no rounding term).  A level-l entry (dX, dY) of a point at (ix, iy)
  * lands at (s_l(ix) + dX, s_l(iy) + dY) (R-A8), and s_l(i) - i lies in (-2^(l-1), 2^(l-1)], so
  * with h = 2^(l-1) the target is within |dX| + h of ix and |dY| + h of iy.  Over the kept list:

@@ -2,8 +2,8 @@
 sums (Eq.(1)): north_star validations V2, V3, V4 plus linearity, translation,
 window additivity and the exact accumulation count.
 
-Non-aligned points under the R-A8 shift rule: parity unpinned beyond these self-consistency
-properties (the paper prints no output values; Fig. 3(b) is a placeholder)."""
+Non-aligned points under the R-A8 shift rule are pinned in tests/test_oracle_shift.py (hand-worked
+s_l(i), the L = 1 closed form, the per-level basis-function synthesis)."""
 import math
 
 import numpy as np
