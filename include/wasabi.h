@@ -66,7 +66,8 @@ typedef struct {
     double retention;     /* r in (0, 1]: N_r,d = min(nnz_d, ceil(r_ppm nnz_d / 1e6)), r_ppm =
                              llround(r 1e6) >= 1 (R-A4; the paper's N_r = pi (W/2)^2 gamma, :92)   */
     int32_t tile;         /* T: bin / superposition tile side; 64 or 128 (multiple of 2^L)        */
-    uint32_t flags;       /* 0, or WASABI_FLAG_EXACT_SHIFT; other bits: EINVAL                      */
+    uint32_t flags;       /* 0, WASABI_FLAG_EXACT_SHIFT or WASABI_FLAG_COIFLET (not both);
+                             other bits: EINVAL                                                    */
 } wasabi_params;
 
 /* Exact off-grid shifts (reading R-A20; needs levels <= 4).  Instead of
@@ -168,13 +169,14 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
 /* ---------------------------------------------------------------- steps 3 (+4) */
 
 /* Step 3: L-level inverse Haar, tile-local (band rows multiples of 2^L, so
- * no halo).  d_u may alias d_psi (in place).  d_u == NULL: u is not written (print only).
+ * no halo).  d_psi is only read in Haar mode (d_u may alias it: in place); it is overwritten in
+ * coiflet mode (below).  d_u == NULL: u is not written (print only).
  * d_bits != NULL fuses step 4 (see wasabi_quantize) and requires `print`.
  * WASABI_FLAG_COIFLET: d_psi is the halo band [max(0, row0 - H), min(n_h, row1 + H)) x n_h
  * (H = wasabi_coif_halo_rows), synthesised IN PLACE (coif1, zero outside the band and the
  * hologram); rows [row0, row1) of the result are u.  d_u (rows [row0, row1)) may be NULL, may be
  * the matching row of d_psi (no copy), or another buffer (copied). */
-wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi, float *d_u, int64_t row0,
+wasabi_status wasabi_inverse_wt(const wasabi_params *params, float *d_psi, float *d_u, int64_t row0,
                                 int64_t row1, const wasabi_print_params *print, uint8_t *d_bits,
                                 cudaStream_t stream);
 

@@ -106,7 +106,14 @@ cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStre
     // large descriptor arrays (thousands of offset-class tables): one stream-ordered copy from the
     // (pageable) host array instead of hundreds of parameter-blob launches; the call returns once
     // the source has been staged, so the caller may free it
-    if (bytes > 16384) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+    // -- but not while the stream is being captured into a CUDA graph: a captured memcpy node would
+    // read the (by then freed) host array at every replay, so under capture the bytes always travel
+    // by value in kernel parameters
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaError_t e = cudaStreamIsCapturing(s, &cap);
+    if (e != cudaSuccess) return e;
+    if (bytes > 16384 && cap == cudaStreamCaptureStatusNone)
+        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
     const unsigned char *p = static_cast<const unsigned char *>(src);
     unsigned char *d = static_cast<unsigned char *>(dst);
     for (size_t off = 0; off < bytes; off += sizeof(Blob::data)) {

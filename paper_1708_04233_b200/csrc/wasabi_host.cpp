@@ -532,7 +532,7 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
     return WASABI_OK;
 }
 
-wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi, float *d_u, int64_t row0,
+wasabi_status wasabi_inverse_wt(const wasabi_params *params, float *d_psi, float *d_u, int64_t row0,
                                 int64_t row1, const wasabi_print_params *print, uint8_t *d_bits, cudaStream_t stream) {
     wasabi_status st = validate(params);
     if (st != WASABI_OK) return st;
@@ -546,7 +546,7 @@ wasabi_status wasabi_inverse_wt(const wasabi_params *params, const float *d_psi,
     if (params->flags & WASABI_FLAG_COIFLET) {   // R-A21: in place on the halo band, then u rows, then bits
         const int64_t H = wasabi_coif_halo_rows(params);
         const int64_t e0 = std::max<int64_t>(0, row0 - H), e1 = std::min<int64_t>(params->n_h, row1 + H);
-        float2 *pe = reinterpret_cast<float2 *>(const_cast<float *>(d_psi));
+        float2 *pe = reinterpret_cast<float2 *>(d_psi);   // coiflets: synthesised in place (wasabi.h)
         if (e1 > e0) CK(launch_coif_inverse(pe, e1 - e0, params->n_h, params->levels, stream), "coif inverse");
         float2 *uc = pe + (row0 - e0) * params->n_h;
         if (d_u && reinterpret_cast<float2 *>(d_u) != uc && row1 > row0)
@@ -702,19 +702,30 @@ wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_pri
     uint8_t *d_bits = reinterpret_cast<uint8_t *>(ws + w.bits);
     // A side stream carries the copies: the points' H2D overlaps the table build, and the bits / u
     // of each row chunk go to the host while the next chunk is superposed (PCIe under the compute).
-    cudaStream_t cs = nullptr;
-    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
-    struct Guard {
-        cudaStream_t s;
-        ~Guard() { cudaStreamDestroy(s); }   // released once its pending work completes
-    } guard{cs};
+    // The copy stream and the join event are created once per host thread and device and reused
+    // (no per-call stream/event creation).
+    struct CopyCtx {
+        int dev = -1;
+        cudaStream_t cs = nullptr;
+        cudaEvent_t ev = nullptr;
+    };
+    thread_local CopyCtx ctx;
+    int dev = 0;
+    CK(cudaGetDevice(&dev), "current device");
+    if (ctx.dev != dev) {
+        if (ctx.cs) cudaStreamDestroy(ctx.cs);   // another device: release the old pair
+        if (ctx.ev) cudaEventDestroy(ctx.ev);
+        ctx.cs = nullptr; ctx.ev = nullptr; ctx.dev = -1;
+        CK(cudaStreamCreateWithFlags(&ctx.cs, cudaStreamNonBlocking), "copy stream");
+        CK(cudaEventCreateWithFlags(&ctx.ev, cudaEventDisableTiming), "join event");
+        ctx.dev = dev;
+    }
+    cudaStream_t cs = ctx.cs;
+    // record + wait are enqueued at once (the wait captures the event's state at the call), so one
+    // event serves every join
     auto join = [&](cudaStream_t waiter, cudaStream_t waited) -> cudaError_t {
-        cudaEvent_t e;
-        cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-        if (r != cudaSuccess) return r;
-        r = cudaEventRecord(e, waited);
-        if (r == cudaSuccess) r = cudaStreamWaitEvent(waiter, e, 0);
-        cudaEventDestroy(e);
+        cudaError_t r = cudaEventRecord(ctx.ev, waited);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(waiter, ctx.ev, 0);
         return r;
     };
     CK(join(cs, stream), "order copy stream");

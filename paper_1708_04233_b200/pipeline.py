@@ -152,6 +152,10 @@ class HologramStream:
             bin_points(self.p, self.tables, points, row0, row1, self.bins, self.stream)
             superpose_inverse(self.p, self.tables, self.bins, row0, row1, self.print_params, None,
                               self.bits[:rows], self.stream)
-            self.h_bits[:rows].copy_(self.bits[:rows], non_blocking=True)
-            torch.cuda.current_stream(self.device).synchronize() if self.stream is None else self.stream.synchronize()
+            # the D2H copy runs on the stream that ran the kernel (ordered after it), and that stream
+            # is synchronised before the host reads h_bits and before the next band reuses self.bits
+            s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+            with torch.cuda.stream(s):
+                self.h_bits[:rows].copy_(self.bits[:rows], non_blocking=True)
+            s.synchronize()
             yield row0, self.h_bits[:rows].numpy().copy()

@@ -6,7 +6,7 @@ quantised direct sum for random (not 2^L-aligned) points."""
 import numpy as np
 import pytest
 
-from helpers import CONFIGS, field_np, gpu_params, make_points, orc_params, rel_l2
+from helpers import field_check, CONFIGS, field_np, gpu_params, make_points, orc_params, rel_l2
 from test_gpu_parity import W, _check_fields, _direct_gpu, _gpu_run, _tables  # noqa: F401
 
 pytestmark = pytest.mark.gpu
@@ -66,7 +66,7 @@ def test_exact_keep_all_equals_gpu_direct_sum_anywhere(W):
     pts = make_points(cfg, n=300)
     _, _, u_w, _ = _gpu_run(W, cfg, pts, 0, 1024, exact=True)
     _, u_d = _direct_gpu(W, cfg, pts, 0, 1024)
-    assert rel_l2(u_w, u_d) <= 1e-5
+    assert max(field_check(u_w, u_d)) <= 1e-5
     _, _, u_s, _ = _gpu_run(W, cfg, pts, 0, 1024)
     assert rel_l2(u_s, u_d) > 1e-2          # control: R-A8 shifts are not exact off-grid
 

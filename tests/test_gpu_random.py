@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from helpers import REF, bits_mismatch_outside_band, field_np, rel_l2
+from helpers import REF, bits_check, field_check, field_np, parity_log, rel_l2
 from test_gpu_parity import W  # noqa: F401
 
 pytestmark = pytest.mark.gpu
@@ -80,6 +80,16 @@ def test_random_problem_parity(W, orc, seed, mode):
         return
     assert rel_l2(psi_g, psi_o) <= 1e-5
     assert rel_l2(u_g, u_o) <= 1e-5
+    e_u, m_u = field_check(u_g, u_o)
+    assert m_u <= 1e-5 and field_check(psi_g, psi_o)[1] <= 1e-5
     bits_o, I_o = orc.quantize(Po, REF, u_o, 0, row0)
-    bad, _, _ = bits_mismatch_outside_band(bits_g, bits_o, I_o, np.abs(u_g - u_o), np.abs(u_o))
-    assert bad == 0
+    bc = bits_check(bits_g, bits_o, I_o, u_g, u_o)
+    parity_log(dict(case=f"random {mode} seed {seed}", rel_u=e_u, max_u=m_u, **bc))
+    assert bc["bad"] == 0, bc
+    if mode != "coif":
+        # the fused entry point (wasabi_superpose_inverse) equals the unfused path bit for bit
+        u_f = torch.zeros_like(pl.field)
+        b_f = torch.zeros_like(pl.bits)
+        W.superpose_inverse(p, pl.tables, pl.bins, row0, row1, pl.print_params, u_f, b_f)
+        torch.cuda.synchronize()
+        assert torch.equal(u_f, pl.field) and torch.equal(b_f, pl.bits)

@@ -156,3 +156,17 @@ def test_accumulation_count_is_sum_of_in_bounds_n_r(orc):
     pts[:, 3] = 1.0
     _, cnt = orc.Lut(P).wasabi_window(pts, 0, 0, 1024, 1024)
     assert cnt == int(geo["n_r"][d].sum())
+
+
+def test_parallel_window_harness_equals_one_window(orc):
+    """helpers.oracle_window (row strips of 2^L rows in a process pool, harness-side point
+    pre-filter) returns exactly the oracle's single-window u, psi and bits."""
+    from helpers import CONFIGS, make_points, oracle_window, orc_params, REF
+    cfg = CONFIGS["C2"]
+    pts = make_points(cfg, n=3000).astype(np.float64)
+    P = orc_params(orc, cfg)
+    u1, psi1, _ = orc.Lut(P).hologram_window(pts, 256, 512, 768, 320)
+    b1, I1 = orc.quantize(P, REF, u1, 256, 512)
+    u2, psi2, b2, I2 = oracle_window(P, pts, 256, 512, 768, 320, procs=4)
+    assert np.array_equal(u1, u2) and np.array_equal(psi1, psi2) and np.array_equal(b1, b2)
+    assert np.array_equal(I1, I2)
