@@ -2,21 +2,24 @@
 """bench.py -- WASABI hot path (arXiv 1708.04233) on B200.
 
 One step = one pass of the whole hot path over the workload: step 1 PSF tables (build), step 2a
-bin, step 2b superpose (Eq.(2)), step 3 inverse Haar fused with step 4 print quantisation (u
-written in place, bits written).  Default workload: BASELINE.json configs[3] (C4: 65,536^2,
-2,000,000 points, 128 levels, L=6, r=5%) on one GPU -- it fits in one B200's HBM.
+bin, steps 2b-4 fused (Eq.(2) superposition, inverse Haar and print quantisation in one kernel; the
+bits are written, u is not).  Default workload: BASELINE.json configs[3] (C4: 65,536^2, 2,000,000
+points, 128 levels, L=6, r=5%) on one GPU -- it fits in one B200's HBM.  `--config C1|C2|C3|C5`
+(+ `--retention`, `--points`) runs the other configs as their own bench lines.
 Under torchrun (N>1) each rank computes one 2^L-aligned row band (strong scaling: the hologram is
-fixed) with no collective in the timed region.
+fixed) with no collective in the timed region; bands are work-balanced by default (`--bands equal`
+for equal heights), and the other partition is timed too and reported beside it.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
 
 `--impl reference` times the fp64 CPU oracle (the tier's reference arm) on a bounded sample of
-the same workload, rank 0 only.  Prints ONE JSON line on rank 0.
+the same workload on all host cores, rank 0 only.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import multiprocessing as mp
 import os
 import statistics
 import subprocess
@@ -31,15 +34,22 @@ from inputs import CONFIGS, make_points  # noqa: E402
 METRIC = "object points/s and hologram Gpixel/s (WASABI superpose+inverse WT), % of HBM roofline"
 UNIT = "Gpixel/s"
 FALLBACK_HBM_GBS = 6650.0
+NOMINAL_FP32_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12     # FFMA lanes x SMs x max SM clock
 
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        hbm = (float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)")
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback"
+        hbm = (FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)")
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2", "fp32_peak.json")) as f:
+            fp = (float(json.load(f)["fp32_tflops"]), "measured (tools/fp32_peak.cu, profiles/r2/fp32_peak.json)")
+    except Exception:
+        fp = (NOMINAL_FP32_TFLOPS, "nominal (2 x 128 FFMA lanes x 148 SMs x 1.965 GHz)")
+    return hbm, fp
 
 
 def _workload(cfg):
@@ -49,44 +59,92 @@ def _workload(cfg):
 
 
 # ----------------------------------------------------------------------------- CPU oracle sample
-def oracle_sample(cfg, pts, window=None, table_depths=None, setup=None):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload and extrapolate to
-    the whole hologram: t = t(sampled depth tables) x (all table area / sampled area) +
-    t(window hot path: bins + Eq.(2) + inverse + quantise) x (N_h^2 / window area)."""
+def _orc_worker(cfg, pts, strip, depths, barrier, q):
+    """One host process of the oracle sample: builds its strip's LUT depths (untimed), then, between
+    barriers, (A) the sampled depth tables and (B) its strip of the window (bins + Eq.(2) + inverse +
+    quantise), reporting the wall-clock of each phase."""
     from oracle import oracle as O
     P = O.Params.from_config(cfg)
-    if setup is None:
-        setup = {}
-        geo = O.geometry(P)
-        setup["area"] = [(2 * int(h)) ** 2 for h in geo["H"]]
-        w = window or min(cfg.n_h, 6144)
-        x0 = y0 = cfg.n_h // 2 - w // 2
-        ix, iy, iz, ok = O.points(P, pts)
-        E = geo["E"][iz]
-        hit = ok & (ix + E >= x0) & (ix - E < x0 + w) & (iy + E >= y0) & (iy - E < y0 + w)
-        lut = O.Lut(P)
-        for d in sorted(set(iz[hit].tolist())):   # untimed: the window's tables are timed separately
-            lut.build_depth(int(d))
-        setup.update(lut=lut, w=w, x0=x0, y0=y0, geo=geo)
-    lut, w, x0, y0 = setup["lut"], setup["w"], setup["x0"], setup["y0"]
-    depths = table_depths if table_depths is not None else [cfg.n_depth // 2, cfg.n_depth - 1]
+    x0, y0, w, h = strip
+    lut = O.Lut(P)
+    lut.hologram_window(pts, x0, y0, w, h)          # untimed: the strip's tables (timed in phase A)
+    barrier.wait()
     t0 = time.perf_counter()
     tl = O.Lut(P)
     for d in depths:
         tl.build_depth(int(d))
-    t_tab = time.perf_counter() - t0
     tl.close()
-    t0 = time.perf_counter()
-    u, _, _ = lut.hologram_window(pts, x0, y0, w, w)
+    t1 = time.perf_counter()
+    barrier.wait()
+    t2 = time.perf_counter()
+    u, _, _ = lut.hologram_window(pts, x0, y0, w, h)
     O.quantize(P, (0.0, 0.030, -0.400), u, x0, y0)
-    t_win = time.perf_counter() - t0
-    area = setup["area"]
-    t_all = t_tab * sum(area) / sum(area[d] for d in depths) + t_win * (cfg.n_h ** 2) / (w * w)
-    sample = (f"oracle (fp64 C, 1 thread): tables of depths {list(depths)} extrapolated by table area to "
-              f"{cfg.n_depth} depths + a {w}x{w} window (bins+Eq.(2)+inverse+quantise) extrapolated to "
-              f"{cfg.n_h}^2; measured {t_tab + t_win:.2f} s, full-hologram estimate {t_all:.1f} s")
-    return dict(value=cfg.n_h ** 2 / t_all / 1e9, unit=UNIT, cores=1, kind="oracle", sample=sample,
-                est_full_s=t_all), setup
+    t3 = time.perf_counter()
+    q.put((t0, t1, t2, t3))
+
+
+def oracle_sample(cfg, pts, procs=1, window=None, table_depths=None):
+    """Time the fp64 oracle (as it stands; the harness only splits the work) on `procs` host
+    processes on a bounded sample of the workload and extrapolate to the whole hologram:
+      t = wall(phase A: sampled depth tables, spread over the processes) x (all table area / sampled)
+        + wall(phase B: a w x w window in row strips of 2^L multiples) x (N_h^2 / window area)."""
+    from oracle import oracle as O
+    P = O.Params.from_config(cfg)
+    geo = O.geometry(P)
+    area = [(2 * int(h)) ** 2 for h in geo["H"]]
+    w = window or min(cfg.n_h, 6144)
+    x0 = y0 = cfg.n_h // 2 - w // 2
+    B = 1 << cfg.levels
+    rows = max(B, (w // procs + B - 1) // B * B)
+    strips = [(x0, y0 + r, w, min(rows, w - r)) for r in range(0, w, rows)]
+    if table_depths is None:
+        table_depths = [cfg.n_depth // 2, cfg.n_depth - 1] if procs == 1 else \
+            [int(round(i * (cfg.n_depth - 1) / max(1, len(strips) - 1))) for i in range(len(strips))]
+    per = [table_depths[i::len(strips)] for i in range(len(strips))]
+    E = int(geo["E"].max()) + 2
+    px = pts[:, 0] / cfg.pitch + cfg.n_h // 2
+    py = pts[:, 1] / cfg.pitch + cfg.n_h // 2
+    ctx = mp.get_context("fork")
+    barrier = ctx.Barrier(len(strips))
+    q = ctx.Queue()
+    ps = []
+    for s, dep in zip(strips, per):
+        m = (px + E >= s[0]) & (px - E < s[0] + s[2]) & (py + E >= s[1]) & (py - E < s[1] + s[3])
+        ps.append(ctx.Process(target=_orc_worker, args=(cfg, pts[m], s, dep, barrier, q)))
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=900) for _ in ps]
+    for p in ps:
+        p.join()
+    t_tab = max(r[1] for r in res) - min(r[0] for r in res)
+    t_win = max(r[3] for r in res) - min(r[2] for r in res)
+    t_all = t_tab * sum(area) / sum(area[d] for d in table_depths) + t_win * (cfg.n_h ** 2) / (w * w)
+    sample = (f"oracle (fp64 C, unchanged) on {len(strips)} host process(es): depth tables {table_depths} "
+              f"extrapolated by table area to {cfg.n_depth} depths + a {w}x{w} window (bins+Eq.(2)+inverse+"
+              f"quantise, row strips of {rows}) extrapolated to {cfg.n_h}^2; measured {t_tab + t_win:.2f} s wall, "
+              f"full-hologram estimate {t_all:.1f} s")
+    return dict(value=cfg.n_h ** 2 / t_all / 1e9, unit=UNIT, cores=len(strips), kind="oracle", sample=sample,
+                est_full_s=t_all)
+
+
+def cpu_baseline(cfg, pts):
+    """The oracle on all host cores (the reported value) and on one thread (context)."""
+    cores = os.cpu_count() or 1
+    allc = oracle_sample(cfg, pts, procs=cores)
+    one = oracle_sample(cfg, pts, procs=1)
+    for d in (allc, one):
+        d.pop("est_full_s", None)
+    allc["single_thread"] = one
+    allc["host"] = _host()
+    return allc
+
+
+def _host():
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        model = "?"
+    return f"{model}, {os.cpu_count()} logical CPUs"
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -133,13 +191,13 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     pts = make_points(cfg)
-    setup = None
-    _, setup = oracle_sample(cfg, pts, table_depths=[cfg.n_depth - 1], setup=None)  # setup (untimed)
+    cores = os.cpu_count() or 1
+    # each step: the all-core oracle sample on another set of sampled depth tables
     vals, tot = [], 0.0
-    sample_depths = [cfg.n_depth - 1, cfg.n_depth // 2, 3 * cfg.n_depth // 4, 0]
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        cb, _ = oracle_sample(cfg, pts, table_depths=[sample_depths[i % len(sample_depths)]], setup=setup)
+        depths = [int((i * 7 + 13 * k) % cfg.n_depth) for k in range(cores)]
+        cb = oracle_sample(cfg, pts, procs=cores, table_depths=depths)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             vals.append(cb)
@@ -148,6 +206,7 @@ def run_reference(args, cfg):
     cb = dict(vals[0])
     cb["value"] = v
     cb.pop("est_full_s", None)
+    cb["host"] = _host()
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / max(1, args.steps),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -162,6 +221,8 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
     import paper_1708_04233_b200 as W
+    from paper_1708_04233_b200.distributed import (assemble_bits, balanced_bands, band_of, band_work, checksums,
+                                                   gather_checksums)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -190,67 +251,113 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def gather(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=cdev)
+        if world == 1:
+            return [vals]
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [p.tolist() for p in parts]
+
     p = W.Params.from_config(cfg)
-    from paper_1708_04233_b200.distributed import band_of, checksums, gather_checksums
-    row0, row1 = band_of(rank, world, cfg.n_h, p.tile)
     pts = make_points(cfg)
     n = len(pts)
     d_pts = torch.from_numpy(pts).to(dev)
-    pl = W.Pipeline(p, n, row0, row1, device=dev)
     stream = torch.cuda.current_stream(dev)
+    scratch8 = torch.zeros(8, dtype=torch.uint8, device=dev)
 
-    for _ in range(args.warmup):
-        pl.run(d_pts, fused=not args.unfused)
-    torch.cuda.synchronize(dev)
-    st = W.bins_stats(pl.bins)
+    # row-work estimate (wasabi_row_work) -> equal and work-balanced bands (host logic, untimed)
+    tb, sb = W.psf_tables_bytes(p)
+    t_tab = torch.empty(tb, dtype=torch.uint8, device=dev)
+    t_scr = torch.empty(sb, dtype=torch.uint8, device=dev)
+    W.build_psf_tables(p, t_tab, t_scr)
+    rw = torch.empty(cfg.n_h + 1, dtype=torch.float64, device=dev)
+    W.row_work(p, t_tab, d_pts, rw, scratch8)
+    row_work = rw[:cfg.n_h].cpu().numpy()
+    eq = [band_of(r, world, cfg.n_h, p.tile) for r in range(world)]
+    bal = balanced_bands(row_work, world, p.tile)
+    mode = args.bands if args.bands else ("balanced" if world > 1 else "equal")
+    parts = {"equal": eq, "balanced": bal}
+    del t_scr, rw
 
-    stages = ["tables", "bin", "superpose", "inverse_quantize"] if args.unfused else \
-        ["tables", "bin", "superpose_inverse_quantize"]
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
-    clocks = Clocks(local, os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
-                    if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_rank{rank}.csv")
-    barrier()
-    torch.cuda.synchronize(dev)
-    clocks.start()
-    time.sleep(0.3)
-    launches0 = W.kernel_launches()
-    for k in range(args.steps):
-        e = ev[k]
-        e[0].record(stream)
-        pl.build_tables()
-        e[1].record(stream)
-        pl.bin(d_pts)
-        e[2].record(stream)
-        if args.unfused:
-            pl.superpose()
-            e[3].record(stream)
-            pl.inverse()
-            e[4].record(stream)
-        else:
-            pl.superpose_inverse()
-            e[3].record(stream)
-    torch.cuda.synchronize(dev)
-    launches = W.kernel_launches() - launches0
-    barrier()
-    ck = clocks.stop()
-    total_ms = sum(ev[k][0].elapsed_time(ev[k][len(stages)]) for k in range(args.steps))
-    stage_ms = {s: statistics.mean(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(args.steps))
-                for i, s in enumerate(stages)}
-    t_ms = max_over_ranks(total_ms)
+    hbm, fp32 = _peaks()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if cfg.n_h < 65536 else None
+
+    def timed_run(bands, steps, warmup, want_clocks):
+        row0, row1 = bands[rank]
+        pl = W.Pipeline(p, n, row0, row1, device=dev)
+        for _ in range(warmup):
+            pl.run(d_pts, fused=not args.unfused)
+        torch.cuda.synchronize(dev)
+        stages = ["tables", "bin", "superpose", "inverse_quantize"] if args.unfused else \
+            ["tables", "bin", "superpose_inverse_quantize"]
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(steps)]
+        clocks = None
+        if want_clocks:
+            clocks = Clocks(local, os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
+                            if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_rank{rank}.csv")
+        barrier()
+        torch.cuda.synchronize(dev)
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        launches0 = W.kernel_launches()
+        for k in range(steps):
+            if flush is not None:
+                flush.zero_()          # L2 flush between timed steps (outside the events)
+            e = ev[k]
+            e[0].record(stream)
+            pl.build_tables()
+            e[1].record(stream)
+            pl.bin(d_pts)
+            e[2].record(stream)
+            if args.unfused:
+                pl.superpose()
+                e[3].record(stream)
+                pl.inverse()
+                e[4].record(stream)
+            else:
+                pl.superpose_inverse()
+                e[3].record(stream)
+        torch.cuda.synchronize(dev)
+        launches = W.kernel_launches() - launches0
+        barrier()
+        ck = clocks.stop() if clocks else None
+        own_ms = sum(ev[k][0].elapsed_time(ev[k][len(stages)]) for k in range(steps))
+        stage_ms = {s: statistics.mean(ev[k][i].elapsed_time(ev[k][i + 1]) for k in range(steps))
+                    for i, s in enumerate(stages)}
+        return pl, own_ms, stage_ms, launches, ck
+
+    bands = parts[mode]
+    row0, row1 = bands[rank]
+    pl, own_ms, stage_ms, launches, ck = timed_run(bands, args.steps, args.warmup, True)
+    t_ms = max_over_ranks(own_ms)
     stage_ms = {s: max_over_ranks(v) for s, v in stage_ms.items()}
     ms_per_step = t_ms / args.steps
     px = cfg.n_h * cfg.n_h
     value = px / (ms_per_step * 1e-3) / 1e9
     points_per_s = n / (ms_per_step * 1e-3)
+    st = W.bins_stats(pl.bins)
+    acc = W.count_accumulations(p, pl.tables, d_pts, row0, row1, scratch8)     # exact Eq.(2) work, untimed
+    per_rank = [dict(rank=i, rows=[int(v[0]), int(v[1])], acc=int(v[2]), ms_per_step=v[3] / args.steps,
+                     est_work=v[4])
+                for i, v in enumerate(gather([row0, row1, acc, own_ms, band_work(row_work, [(row0, row1)])[0]]))]
 
-    # checksum assembly after the timed region (the only collective: NCCL all_gather)
-    cs = checksums(pl.field, pl.bits)
+    # checksums and assembly of the print bits after the timed region (the only collectives)
+    cs = checksums(None, pl.bits).to(cdev)
+    assembled = None
     if world > 1:
-        cs = gather_checksums(cs.to(cdev)).sum(dim=0)
+        cs_all = gather_checksums(cs)
+        full = assemble_bits(pl.bits.to(cdev), cfg.n_h, p.tile, bands=bands)
+        table = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.float64, device=full.device)
+        assembled = {"rows": int(full.shape[0]), "bits_set": float(table[full.reshape(-1).long()].sum()),
+                     "band_bits_set_sum": float(cs_all[:, 3].sum())}
+        cs = cs_all.sum(dim=0)
+        del full
     cs = cs.tolist()
 
-    # roofline of the dominant kernel (algorithmic bytes per launch / event-timed duration)
-    peak, peak_src = _peaks()
+    # roofline of the dominant kernel: HBM (algorithmic bytes per launch / event-timed duration) and
+    # FP32 (4 flops per Eq.(2) accumulation, exact count) against the measured peaks
     rows = row1 - row0
     alg = {"superpose": 8.0 * rows * cfg.n_h + 16.0 * st["n_valid"],
            "inverse_quantize": 16.125 * rows * cfg.n_h,
@@ -258,41 +365,56 @@ def run_ours(args, cfg):
            "bin": 16.0 * n + 16.0 * st["n_valid"] + 8.0 * st["entries"],
            "tables": 0.0}
     dom = max(stage_ms, key=stage_ms.get)
-    # per-launch DRAM traffic and on-chip limiter of the dominant kernel, from one committed
-    # `ncu --set full` capture of this same workload (tools/ncu_traffic.py -> profiles/ncu_traffic.json)
     traffic, onchip = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and cfg.name == "C4" and args.retention is None and args.points is None:
         try:
             rec = json.load(open(tpath)).get(dom)
             if isinstance(rec, dict):
-                traffic = rec.get("traffic")
-                onchip = rec.get("onchip")
+                traffic, onchip = rec.get("traffic"), rec.get("onchip")
                 prof_rows = rec.get("rows")
-                if traffic is not None and prof_rows and prof_rows != rows and cfg.name == "C4":
-                    # the capture is of the full hologram; a band moves its share of it
-                    traffic = traffic * rows / prof_rows
+                if traffic is not None and prof_rows and prof_rows != rows:
+                    traffic = traffic * rows / prof_rows      # the capture is of the full hologram
                     onchip = dict(onchip or {}, traffic_scaled_from_rows=prof_rows)
-                elif cfg.name != "C4":
-                    traffic, onchip = None, None   # the capture is of C4 only
-            else:
-                traffic = rec
         except Exception:
             traffic = None
     ach = alg[dom] / (stage_ms[dom] * 1e-3) / 1e9 if alg[dom] else 0.0
     step_bytes = (24.125 if args.unfused else 8.125) * rows * cfg.n_h + 32.0 * n
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm[0], "unit": "GB/s",
+                "frac": ach / hbm[0], "traffic": traffic, "peak_source": hbm[1],
+                "alg_bytes_per_launch": alg[dom],
                 "step_achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,
-                "step_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak}
+                "step_frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / hbm[0]}
+    sup = "superpose" if args.unfused else "superpose_inverse_quantize"
+    fl = 4.0 * acc / (stage_ms[sup] * 1e-3) / 1e12
+    roofline["fp32"] = {"kernel": sup, "accumulations": acc, "flops_per_accumulation": 4,
+                        "achieved": fl, "peak": fp32[0], "unit": "TFLOP/s", "frac": fl / fp32[0],
+                        "peak_source": fp32[1],
+                        "acc_per_s": acc / (stage_ms[sup] * 1e-3)}
     if onchip:
         roofline["onchip"] = onchip
+
+    # the other band partition, timed the same way (N > 1 only)
+    alt = None
+    if world > 1 and not args.no_alt_bands:
+        other = "equal" if mode == "balanced" else "balanced"
+        del pl
+        torch.cuda.empty_cache()
+        pl2, own2, _, _, _ = timed_run(parts[other], args.steps, 1, False)
+        acc2 = W.count_accumulations(p, pl2.tables, d_pts, *parts[other][rank], scratch8)
+        g2 = gather([own2, acc2])
+        t2 = max(v[0] for v in g2) / args.steps
+        alt = {"bands": other, "ms_per_step": t2, "value": px / (t2 * 1e-3) / 1e9,
+               "per_rank": [dict(rank=i, rows=list(parts[other][i]), acc=int(v[1]), ms_per_step=v[0] / args.steps)
+                            for i, v in enumerate(g2)]}
+        del pl2
+    else:
+        del pl
+    torch.cuda.empty_cache()
 
     # end-to-end through the C ABI with host buffers (H2D points + whole path + D2H bits)
     e2e = None
     if not args.no_e2e:
-        del pl
-        torch.cuda.empty_cache()
         ws = torch.empty(W.hologram_workspace_bytes(p, n, row0, row1), dtype=torch.uint8, device=dev)
         h_pts = torch.from_numpy(pts).pin_memory()
         h_bits = torch.empty((rows, cfg.n_h // 8), dtype=torch.uint8).pin_memory()
@@ -301,34 +423,41 @@ def run_ours(args, cfg):
             W.hologram_host(p, pr, h_pts, row0, row1, ws, h_bits, None, stream)
         torch.cuda.synchronize(dev)
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        te_sum = 0.0
         for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             W.hologram_host(p, pr, h_pts, row0, row1, ws, h_bits, None, stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        te = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            te_sum += e0.elapsed_time(e1)
+        te = max_over_ranks(te_sum) / args.steps
         e2e = {"value": px / (te * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": te,
                "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": rows * (cfg.n_h // 8)}
         del ws
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, _ = oracle_sample(cfg, pts)
-        cpu.pop("est_full_s", None)
+        cpu = cpu_baseline(cfg, pts)
 
     if rank == 0:
+        l2 = ("inputs larger than L2 (bits 0.5 GB, bins 0.6 GB, tables 0.45 GB per step)" if flush is None else
+              "L2 flushed between timed steps (256 MB write outside the events)")
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded generators, inputs/; the paper's 3D model is unavailable)",
-               "config": {"workload": _workload(cfg), "path": "unfused" if args.unfused else "fused", "n_h": cfg.n_h, "n_points": n, "levels": cfg.levels,
-                          "retention": cfg.retention, "n_depth": cfg.n_depth, "tile": p.tile,
-                          "rows_per_gpu": rows, "parallelism": f"row bands x{world}",
-                          "l2": f"inputs larger than L2 (psi/u {8 * rows * cfg.n_h / 1e9:.1f} GB per GPU per step)"},
+               "config": {"workload": _workload(cfg), "path": "unfused" if args.unfused else "fused",
+                          "n_h": cfg.n_h, "n_points": n, "levels": cfg.levels, "retention": cfg.retention,
+                          "n_depth": cfg.n_depth, "tile": p.tile, "rows_per_gpu": rows,
+                          "parallelism": f"row bands x{world} ({mode})", "l2": l2},
                "points_per_s": points_per_s, "stage_ms": stage_ms, "bin_entries": st["entries"],
+               "accumulations": sum(r["acc"] for r in per_rank),
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-               "clocks": ck, "checksum": {"u_energy": cs[0], "u_re_sum": cs[1], "u_im_sum": cs[2], "bits_set": cs[3]},
+               "clocks": ck, "per_rank": per_rank, "bands_alt": alt, "assembled": assembled,
+               "checksum": {"bits_set": cs[3]},
                "paper_context": {"wasabi_s_65536sq_95949pts_cpu": 354, "nlut_s": 10533,
                                  "cite": "PAPER.md:166 (Xeon E5 v3; different point count and wavelet)"}}
         print(json.dumps(out), flush=True)
@@ -344,7 +473,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--points", type=int, default=None, help="override the config's point count")
+    ap.add_argument("--retention", type=float, default=None, help="override the config's r")
     ap.add_argument("--tile", type=int, default=None)
+    ap.add_argument("--bands", default=None, choices=["equal", "balanced"],
+                    help="row-band partition (default: balanced for N > 1)")
+    ap.add_argument("--no-alt-bands", action="store_true", help="N > 1: skip timing the other partition")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="time the 4-call path (psi through HBM)")
@@ -354,6 +487,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.points:
         cfg = cfg.replace(n_points=args.points)
+    if args.retention:
+        cfg = cfg.replace(retention=args.retention)
     if args.tile:
         cfg = cfg.replace(tile=args.tile)
     if args.impl == "reference":

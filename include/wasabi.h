@@ -203,6 +203,25 @@ wasabi_status wasabi_build_psf_dense(const wasabi_params *params, void *d_dense,
 wasabi_status wasabi_direct_sum(const wasabi_params *params, const void *d_dense, const void *d_bins, int64_t row0,
                                 int64_t row1, float *d_u, cudaStream_t stream);
 
+/* ---------------------------------------------------------------- work accounting (not the hot path) */
+
+/* The exact number of Eq.(2) accumulations whose target lies in the hologram
+ * and in rows [row0, row1): sum over valid points j of the kept coefficients (l, X, Y) of the point's
+ * table with (s_l(ix_j) + X - H, s_l(iy_j) + Y - H) inside (R-A8; R-A20 shifts in exact mode) --
+ * the work a band's superposition does (4 fp32 flops each).  d_scratch: >= 8 bytes of device
+ * memory.  SYNCHRONOUS (one 8-byte device->host read); one warp per point walks its kept list. */
+wasabi_status wasabi_count_accumulations(const wasabi_params *params, const void *d_tables, const float *d_points,
+                                        int64_t n, int64_t row0, int64_t row1, void *d_scratch, int64_t *h_count,
+                                        cudaStream_t stream);
+
+/* Per-row work estimate for work-balanced row bands (PAPER.md:115-125 sub-holograms):
+ * every valid point's in-hologram accumulation count, spread uniformly over its reach rows
+ * [iy - Ek, iy + Ek] (R-A19) and clipped to the hologram.  d_row_work: n_h + 1 doubles (device);
+ * on completion d_row_work[Y] (Y < n_h) is the estimated work of row Y (entry n_h is scratch).
+ * d_scratch >= 8 bytes.  Asynchronous. */
+wasabi_status wasabi_row_work(const wasabi_params *params, const void *d_tables, const float *d_points, int64_t n,
+                              double *d_row_work, void *d_scratch, cudaStream_t stream);
+
 /* ---------------------------------------------------------------- whole path, host buffers */
 
 /* Device workspace for wasabi_hologram_host (tables + scratch + points + bins + field). */

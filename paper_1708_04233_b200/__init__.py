@@ -127,6 +127,8 @@ def lib() -> C.CDLL:
             "wasabi_export_bins": [_PP, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
             "wasabi_export_reach": [_PP, _vp, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
             "wasabi_bins_stats": [_vp, C.POINTER(_i64 * 8)],
+            "wasabi_count_accumulations": [_PP, _vp, _vp, _i64, _i64, _i64, _vp, C.POINTER(_i64), _vp],
+            "wasabi_row_work": [_PP, _vp, _vp, _i64, _vp, _vp, _vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -249,6 +251,21 @@ def build_psf_dense(p: Params, dense, stream=None):
 def direct_sum(p: Params, dense, bins, row0: int, row1: int, u, stream=None):
     """Quantised direct sum of Eq.(1) (PSF stamping; the paper's conventional method) for a band."""
     _check(lib().wasabi_direct_sum(C.byref(p.c()), _ptr(dense), _ptr(bins), row0, row1, _ptr(u), _stream(stream)))
+
+
+# ----------------------------------------------------------------------------- work accounting
+def count_accumulations(p: Params, tables, points, row0: int, row1: int, scratch, stream=None) -> int:
+    """Exact Eq.(2) accumulation count of rows [row0, row1) (synchronous; scratch >= 8 device bytes)."""
+    n = _i64()
+    _check(lib().wasabi_count_accumulations(C.byref(p.c()), _ptr(tables), _ptr(points), points.shape[0], row0,
+                                            row1, _ptr(scratch), C.byref(n), _stream(stream)))
+    return n.value
+
+
+def row_work(p: Params, tables, points, out, scratch, stream=None):
+    """Per-row work estimate into `out` (n_h + 1 float64 device tensor; out[:n_h] meaningful)."""
+    _check(lib().wasabi_row_work(C.byref(p.c()), _ptr(tables), _ptr(points), points.shape[0], _ptr(out),
+                                 _ptr(scratch), _stream(stream)))
 
 
 # ----------------------------------------------------------------------------- whole path

@@ -165,6 +165,13 @@ cudaError_t launch_bin(const BinHeader &bh, void *d_bins, const KDesc *kd, const
                        double pitch, int64_t n_h, double z_min, double dz, int n_depth, int cls_bits,
                        cudaStream_t s);
 
+// Eq.(2) accumulation count of band [row0, row1) into *d_count (device u64) and, if d_row_work !=
+// NULL (n_h + 1 doubles), the per-row work estimate of the balanced bands (inclusive prefix sums of
+// a difference array, scanned: [Y] = work of row Y for Y < n_h).  h: the host copy of the table header.
+cudaError_t launch_count_acc(const TableHeader &h, const void *d_tables, const float4 *pts, int64_t n, double pitch,
+                             int64_t n_h, double z_min, double dz, int n_depth, int cls_bits, int L, int64_t row0,
+                             int64_t row1, unsigned long long *d_count, double *d_row_work, cudaStream_t s);
+
 // fused = 0: write psi; fused = 1: inverse Haar in shared memory, write u (psi pointer, may be NULL)
 // and, if bits != NULL, the print bits (print4 = {xr, yr, zr, 1/lambda}).
 // tile rows [tile_row0, tile_row1) of the bins' band (tile_row1 < 0: all)

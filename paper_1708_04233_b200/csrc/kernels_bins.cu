@@ -256,7 +256,109 @@ __global__ void finish_kernel(BinHeader *bh, const unsigned long long *ptr, int6
     if (ptr[n_tiles] > (unsigned long long)bh->capacity) bh->status = 1;
 }
 
+// ---- Eq.(2) accumulation count and per-row work (diagnostics / band balancing, not the hot path) ----
+// One warp per point: the lanes walk the point's canonical kept list (16-byte entries, X | Y << 14 |
+// l << 28) and count the targets (s + X - H, s + Y - H) inside [0, n_h) x [row0, row1), s the point's
+// shift (R-A8 standard: s_l(i) = 2^l floor((i + 2^(l-1)) / 2^l); R-A20 exact: i with the class bits
+// cleared) -- the exact number of Eq.(2) accumulations of the band.  With row_diff != NULL the
+// point's full-hologram count is also spread uniformly over its reach rows [iy - Ek, iy + Ek] of a
+// difference array (the work model of the balanced row bands).
+__global__ void __launch_bounds__(256) count_acc_kernel(const float4 *__restrict__ pts, BinArgs A,
+                                                        const KDesc *__restrict__ kd, const DDesc *__restrict__ dd,
+                                                        const int32_t *__restrict__ gptr,
+                                                        const uint4 *__restrict__ ent, int L,
+                                                        unsigned long long *__restrict__ count,
+                                                        double *__restrict__ row_diff) {
+    const int lane = threadIdx.x & 31;
+    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (j >= A.n) return;
+    int ix = 0, iy = 0, iz = 0;
+    if (!convert_point(pts[j], A, ix, iy, iz)) return;
+    const int t = table_of(ix, iy, iz, A.cls_bits);
+    const int H = kd[t].H;
+    const int e0 = gptr[dd[t].group_base], e1 = gptr[dd[t].group_base + dd[t].n_groups];
+    const int cm = (1 << A.cls_bits) - 1;
+    unsigned long long band = 0, full = 0;
+    for (int e = e0 + lane; e < e1; e += 32) {
+        const uint32_t w = ent[e].x;
+        const int X = (int)(w & 0x3fffu), Y = (int)((w >> 14) & 0x3fffu), l = (int)(w >> 28);
+        const int h = 1 << (l - 1);
+        const long long sx = A.cls_bits ? (ix & ~cm) : floor_div((long long)ix + h, 1LL << l) << l;
+        const long long sy = A.cls_bits ? (iy & ~cm) : floor_div((long long)iy + h, 1LL << l) << l;
+        const long long Xh = sx + X - H, Yh = sy + Y - H;
+        if (Xh >= 0 && Xh < A.n_h && Yh >= 0 && Yh < A.n_h) {
+            full++;
+            if (Yh >= A.row0 && Yh < A.row1) band++;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        band += __shfl_xor_sync(0xffffffffu, band, o);
+        full += __shfl_xor_sync(0xffffffffu, full, o);
+    }
+    if (lane == 0) {
+        if (band) atomicAdd(count, band);
+        if (row_diff && full) {
+            const int ek = kd[t].Ek;
+            const long long y0 = max(0LL, (long long)iy - ek), y1 = min((long long)A.n_h - 1, (long long)iy + ek);
+            if (y1 >= y0) {
+                const double wrow = (double)full / (double)(y1 - y0 + 1);
+                atomicAdd(&row_diff[y0], wrow);
+                atomicAdd(&row_diff[y1 + 1], -wrow);
+            }
+        }
+    }
+}
+
+// In-place inclusive scan of n doubles by one CTA (the per-row work array: n = N_h <= 2^17).
+__global__ void __launch_bounds__(1024) scan_rows_kernel(double *__restrict__ a, int64_t n) {
+    __shared__ double part[1024];
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t b = threadIdx.x * per, e = min(n, b + per);
+    double s = 0.0;
+    for (int64_t i = b; i < e; i++) s += a[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const double v = threadIdx.x >= o ? part[threadIdx.x - o] : 0.0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    double c = threadIdx.x ? part[threadIdx.x - 1] : 0.0;
+    for (int64_t i = b; i < e; i++) {
+        c += a[i];
+        a[i] = c;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_count_acc(const TableHeader &h, const void *d_tables, const float4 *pts, int64_t n, double pitch,
+                             int64_t n_h, double z_min, double dz, int n_depth, int cls_bits, int L, int64_t row0,
+                             int64_t row1, unsigned long long *d_count, double *d_row_work, cudaStream_t s) {
+    const char *tb = static_cast<const char *>(d_tables);
+    cudaError_t e;
+    BinArgs A;
+    A.n = n; A.n_h = n_h; A.row0 = row0; A.row1 = row1;
+    A.T = h.tile; A.tiles_x = 0; A.tiles_y = 0; A.n_depth = n_depth; A.cls_bits = cls_bits;
+    A.pitch = pitch; A.z_min = z_min; A.dz = dz;
+    if ((e = cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+    if (d_row_work && (e = cudaMemsetAsync(d_row_work, 0, sizeof(double) * (size_t)(n_h + 1), s)) != cudaSuccess)
+        return e;
+    if (n > 0) {
+        count_launches(1);
+        count_acc_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, s>>>(
+            pts, A, reinterpret_cast<const KDesc *>(tb + h.kdesc_off), reinterpret_cast<const DDesc *>(tb + h.ddesc_off),
+            reinterpret_cast<const int32_t *>(tb + h.ptr_off), reinterpret_cast<const uint4 *>(tb + h.ent_off), L,
+            d_count, d_row_work);
+    }
+    if (d_row_work) {
+        count_launches(1);
+        scan_rows_kernel<<<1, 1024, 0, s>>>(d_row_work, n_h);
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_bin(const BinHeader &h, void *d_bins, const KDesc *kd, const float4 *pts, double pitch,
                        int64_t n_h, double z_min, double dz, int n_depth, int cls_bits, cudaStream_t s) {

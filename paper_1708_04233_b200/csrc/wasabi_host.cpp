@@ -493,6 +493,43 @@ wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_table
     return WASABI_OK;
 }
 
+wasabi_status wasabi_count_accumulations(const wasabi_params *params, const void *d_tables, const float *d_points,
+                                        int64_t n, int64_t row0, int64_t row1, void *d_scratch, int64_t *h_count,
+                                        cudaStream_t stream) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if (row0 < 0 || row1 > params->n_h || row1 < row0) return fail(WASABI_EINVAL, "rows out of range");
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(WASABI_EINVAL, "n out of range");
+    if (!d_tables || !d_scratch || !h_count || (n > 0 && !d_points)) return fail(WASABI_EINVAL, "NULL buffer");
+    if (!aligned(d_scratch, 8) || (n > 0 && !aligned(d_points, 16))) return fail(WASABI_EINVAL, "misaligned buffer");
+    unsigned long long *cnt = static_cast<unsigned long long *>(d_scratch);
+    CK(launch_count_acc(g.th, d_tables, reinterpret_cast<const float4 *>(d_points), n, params->pitch_m, params->n_h,
+                        params->z_min_m, g.dz, g.nz, g.cb, g.L, row0, row1, cnt, nullptr, stream),
+       "count accumulations");
+    unsigned long long c = 0;
+    CK(cudaMemcpyAsync(&c, cnt, sizeof c, cudaMemcpyDeviceToHost, stream), "read count");
+    CK(cudaStreamSynchronize(stream), "sync");
+    *h_count = (int64_t)c;
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_row_work(const wasabi_params *params, const void *d_tables, const float *d_points, int64_t n,
+                              double *d_row_work, void *d_scratch, cudaStream_t stream) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if (n < 0 || n > (int64_t)INT32_MAX) return fail(WASABI_EINVAL, "n out of range");
+    if (!d_tables || !d_scratch || !d_row_work || (n > 0 && !d_points)) return fail(WASABI_EINVAL, "NULL buffer");
+    if (!aligned(d_scratch, 8) || !aligned(d_row_work, 8) || (n > 0 && !aligned(d_points, 16)))
+        return fail(WASABI_EINVAL, "misaligned buffer");
+    CK(launch_count_acc(g.th, d_tables, reinterpret_cast<const float4 *>(d_points), n, params->pitch_m, params->n_h,
+                        params->z_min_m, g.dz, g.nz, g.cb, g.L, 0, params->n_h,
+                        static_cast<unsigned long long *>(d_scratch), d_row_work, stream),
+       "row work");
+    return WASABI_OK;
+}
+
 wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables, const void *d_bins, int64_t row0,
                                int64_t row1, float *d_psi, cudaStream_t stream) {
     wasabi_status st = validate(params);

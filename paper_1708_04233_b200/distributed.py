@@ -6,7 +6,7 @@ is no collective in the data path: bands are independent.
 """
 from __future__ import annotations
 
-from typing import Tuple
+from typing import List, Optional, Tuple
 
 
 def band_of(rank: int, world: int, n_h: int, align: int) -> Tuple[int, int]:
@@ -23,6 +23,40 @@ def band_of(rank: int, world: int, n_h: int, align: int) -> Tuple[int, int]:
     start = rank * base + max(0, rank - first_big)
     count = base + (1 if rank >= first_big else 0)
     return start * align, (start + count) * align
+
+
+def balanced_bands(row_work, world: int, align: int) -> List[Tuple[int, int]]:
+    """Work-balanced row bands (SURVEY.md §8(e) load balance; PAPER.md:115-125 sub-holograms): edges
+    are multiples of `align` (tile, 2^L) chosen so each band's share of sum(row_work) is as close as
+    possible to total/world.  `row_work` is the per-row work estimate of wasabi_row_work (length
+    n_h).  Edge k is the aligned row nearest to the row where the work prefix reaches k/world of the
+    total, kept strictly increasing (every band at least one aligned block).  Host logic only."""
+    import numpy as np
+    w = np.asarray(row_work, dtype=np.float64)
+    n_h = w.shape[0]
+    if world < 1 or n_h % align or n_h // align < world:
+        raise ValueError("bad world / align for balanced bands")
+    blocks = n_h // align
+    cum = np.concatenate([[0.0], np.cumsum(w.reshape(blocks, align).sum(axis=1))])   # work before block b
+    tot = cum[-1]
+    edges = [0]
+    for k in range(1, world):
+        if tot > 0:
+            b = int(np.searchsorted(cum, tot * k / world))
+            b = b if b == 0 or abs(cum[b] - tot * k / world) <= abs(cum[b - 1] - tot * k / world) else b - 1
+        else:
+            b = round(blocks * k / world)
+        b = min(max(b, edges[-1] + 1), blocks - (world - k))
+        edges.append(b)
+    edges.append(blocks)
+    return [(edges[r] * align, edges[r + 1] * align) for r in range(world)]
+
+
+def band_work(row_work, bands) -> List[float]:
+    """Sum of the per-row work estimate over each band."""
+    import numpy as np
+    w = np.asarray(row_work, dtype=np.float64)
+    return [float(w[b0:b1].sum()) for b0, b1 in bands]
 
 
 def checksums(u, bits):
@@ -56,13 +90,15 @@ def gather_checksums(local, group=None):
     return torch.stack(parts)
 
 
-def assemble_bits(local_bits, n_h: int, align: int, group=None):
+def assemble_bits(local_bits, n_h: int, align: int, group=None, bands: Optional[List[Tuple[int, int]]] = None):
     """Gather every rank's band of print bits into the full (n_h, n_h/8) pattern (all ranks get it).
-    Bands may differ in height, so each is padded to the largest band for the collective."""
+    `bands` (default: the equal bands of band_of) lists every rank's [row0, row1); bands may differ
+    in height, so each is padded to the largest band for the collective."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    bands = [band_of(r, world, n_h, align) for r in range(world)]
+    if bands is None:
+        bands = [band_of(r, world, n_h, align) for r in range(world)]
     hmax = max(b1 - b0 for b0, b1 in bands)
     pad = torch.zeros((hmax, n_h // 8), dtype=torch.uint8, device=local_bits.device)
     pad[: local_bits.shape[0]] = local_bits

@@ -514,3 +514,28 @@ def test_cuda_graph_replay_equals_eager(W, kw):
         torch.cuda.synchronize()
         assert torch.equal(pl.bits, eager.bits)
         assert torch.equal(pl.field, eager.field)
+
+
+# ---------------------------------------------------------------- work accounting
+@pytest.mark.parametrize("name,n,row0,row1,kw", [("C2", 3000, 512, 1024, {}), ("C1", None, 0, 512, {}),
+                                                 ("C1", 500, 128, 320, dict(exact=True)),
+                                                 ("C3", 20000, 4096, 4608, {})])
+def test_count_accumulations_equals_oracle(W, orc, name, n, row0, row1, kw):
+    """wasabi_count_accumulations == the number of in-window accumulations the oracle's Eq.(2)
+    performs on the full-width band (orc_wasabi_window's count), exactly; the row-work estimate sums
+    to the full-hologram count."""
+    import torch
+    cfg = CONFIGS[name]
+    pts = make_points(cfg, n=n)
+    p = gpu_params(cfg, **kw)
+    t = _tables(W, p)
+    d = torch.from_numpy(pts).cuda()
+    s8 = torch.zeros(8, dtype=torch.uint8, device="cuda")
+    got = W.count_accumulations(p, t, d, row0, row1, s8)
+    P = orc_params(orc, cfg, **kw)
+    _, cnt = orc.Lut(P).wasabi_window(pts, 0, row0, cfg.n_h, row1 - row0)
+    assert got == cnt
+    rw = torch.empty(cfg.n_h + 1, dtype=torch.float64, device="cuda")
+    W.row_work(p, t, d, rw, s8)
+    full = W.count_accumulations(p, t, d, 0, cfg.n_h, s8)
+    assert abs(float(rw[:cfg.n_h].sum()) - full) <= 1e-6 * full

@@ -10,7 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1708_04233_b200.distributed import assemble_bits, band_of, checksums, gather_checksums
+from paper_1708_04233_b200.distributed import (assemble_bits, balanced_bands, band_of, band_work, checksums,
+                                               gather_checksums)
 
 
 def test_band_partition_properties():
@@ -37,7 +38,44 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_q):
+def _oracle_row_work(orc, P, pts):
+    """Host-side stand-in for wasabi_row_work (test only): each valid point's kept-list size spread
+    uniformly over its reach rows [iy - ek, iy + ek] (R-A19), from the oracle's points and reach."""
+    ix, iy, iz, ok = orc.points(P, pts)
+    ek, _ = orc.reach(P)
+    nr = orc.geometry(P)["n_r"]
+    diff = np.zeros(P.n_h + 1)
+    for y, d, v in zip(iy, iz, ok):
+        if not v:
+            continue
+        y0, y1 = max(0, y - ek[d]), min(P.n_h - 1, y + ek[d])
+        if y1 >= y0:
+            diff[y0] += nr[d] / (y1 - y0 + 1)
+            diff[y1 + 1] -= nr[d] / (y1 - y0 + 1)
+    return np.cumsum(diff)[:P.n_h]
+
+
+def test_balanced_bands_properties():
+    """Balanced bands tile [0, N_h) with aligned, strictly increasing edges, and even out a skewed
+    work profile far better than equal bands."""
+    rng = np.random.default_rng(3)
+    for n_h, align, world in [(512, 64, 2), (512, 64, 4), (65536, 64, 8), (2048, 128, 3), (8192, 64, 8)]:
+        w = rng.random(n_h) ** 4 * 10
+        w[: n_h // 8] *= 20                      # a dense top strip
+        bands = balanced_bands(w, world, align)
+        assert bands[0][0] == 0 and bands[-1][1] == n_h
+        for (a0, a1), (b0, b1) in zip(bands, bands[1:]):
+            assert a1 == b0
+        for b0, b1 in bands:
+            assert b0 % align == 0 and b1 % align == 0 and b1 > b0
+        if n_h // align >= 8 * world:
+            bw, ew = band_work(w, bands), band_work(w, [band_of(r, world, n_h, align) for r in range(world)])
+            assert max(bw) / np.mean(bw) < max(ew) / np.mean(ew)
+    assert balanced_bands(np.zeros(512), 2, 64) == [(0, 256), (256, 512)]
+    assert balanced_bands(np.ones(512), 8, 64) == [(64 * r, 64 * (r + 1)) for r in range(8)]
+
+
+def _worker(rank, world, port, bands, out_q):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -49,12 +87,12 @@ def _worker(rank, world, port, out_q):
     cfg = CONFIGS["C1"]
     P = O.Params.from_config(cfg)
     pts = make_points(cfg, n=400)
-    r0, r1 = band_of(rank, world, cfg.n_h, cfg.tile)
+    r0, r1 = bands[rank]
     u, _, _ = O.Lut(P).hologram_window(pts, 0, r0, cfg.n_h, r1 - r0)     # band compute (oracle)
     bits, _ = O.quantize(P, (0.0, 0.030, -0.400), u, 0, r0)
     tb = torch.from_numpy(bits)
     tu = torch.from_numpy(np.stack([u.real, u.imag], -1))
-    full = assemble_bits(tb, cfg.n_h, cfg.tile)
+    full = assemble_bits(tb, cfg.n_h, cfg.tile, bands=bands)
     cs = gather_checksums(checksums(tu, tb))
     if rank == 0:
         out_q.put((full.numpy(), cs.numpy()))
@@ -62,22 +100,29 @@ def _worker(rank, world, port, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_two_rank_assembly_equals_single_band(world, orc):
+@pytest.mark.parametrize("world,kind", [(2, "equal"), (2, "balanced"), (4, "balanced")])
+def test_rank_assembly_equals_single_band(world, kind, orc):
+    """world-2/4 gloo: every rank computes its band (equal, or work-balanced from the row-work
+    estimate); the assembled print bits equal the single-band hologram bit for bit, and the band
+    checksums add up to the single band's."""
     from inputs import CONFIGS, make_points
+    cfg = CONFIGS["C1"]
+    P = orc.Params.from_config(cfg)
+    pts = make_points(cfg, n=400)
+    if kind == "equal":
+        bands = [band_of(r, world, cfg.n_h, cfg.tile) for r in range(world)]
+    else:
+        bands = balanced_bands(_oracle_row_work(orc, P, pts), world, cfg.tile)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, bands, q)) for r in range(world)]
     for p in procs:
         p.start()
     full, cs = q.get(timeout=300)
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
-    cfg = CONFIGS["C1"]
-    P = orc.Params.from_config(cfg)
-    pts = make_points(cfg, n=400)
     u, _, _ = orc.Lut(P).hologram_window(pts, 0, 0, cfg.n_h, cfg.n_h)
     bits, _ = orc.quantize(P, (0.0, 0.030, -0.400), u, 0, 0)
     assert np.array_equal(full, bits)

@@ -32,6 +32,10 @@ rec = {"traffic": traffic,
                   "shared_bank_conflict_wavefronts": num("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
                   "shared_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
                   "l2_hit_rate": float(d["lts__t_sector_hit_rate.pct"]) / 100.0,
+                  "fma_pipe_frac": float(d["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]) / 100.0,
+                  "fp64_pipe_frac": float(d["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]) / 100.0,
+                  "issue_active_frac": float(d["sm__issue_active.avg.pct_of_peak_sustained_elapsed"]) / 100.0,
+                  "warp_instructions": num("smsp__inst_executed.sum") if "smsp__inst_executed.sum" in d else None,
                   "source": f"ncu --set full, {os.path.basename(rep)}"},
        "kernel": d.get("Kernel Name", "")[:80], "duration_ms_under_ncu": num("gpu__time_duration.sum") / 1e6
        if units[hdr.index("gpu__time_duration.sum")] == "nsecond" else float(d["gpu__time_duration.sum"])}
