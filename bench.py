@@ -391,6 +391,14 @@ def run_ours(args, cfg):
                         "achieved": fl, "peak": fp32[0], "unit": "TFLOP/s", "frac": fl / fp32[0],
                         "peak_source": fp32[1],
                         "acc_per_s": acc / (stage_ms[sup] * 1e-3)}
+    # on-chip ceiling of the scatter: one 64-bit shared read-modify-write per
+    # accumulation, 32 lanes x 8 B = two 128-B wavefronts per LDS.64 and per STS.64, one wavefront per
+    # clock per SM -> 8 accumulations / clock / SM at zero bank conflicts
+    f_sm = (ck or {}).get("sm_max_mhz") or 1965.0
+    ceil_acc = 148 * f_sm * 1e6 * 8
+    roofline["onchip_acc"] = {"kernel": sup, "achieved": acc / (stage_ms[sup] * 1e-3), "peak": ceil_acc,
+                              "unit": "accumulations/s", "frac": acc / (stage_ms[sup] * 1e-3) / ceil_acc,
+                              "peak_source": "148 SMs x f_SM x 8 acc/clk (shared-memory RMW, conflict-free)"}
     if onchip:
         roofline["onchip"] = onchip
 
@@ -465,6 +473,77 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- conventional method
+def run_direct(args, cfg):
+    """The paper's comparison (WASABI ~30x faster than the conventional method on
+    a CPU) on this GPU: per step the conventional method -- dense PSF tables, bins by the whole PSF disc,
+    the quantised direct sum of Eq.(1) by PSF stamping (wasabi_direct_sum) and the same print
+    quantisation -- timed against the WASABI step on the same points, CUDA events, one GPU."""
+    import torch
+    import paper_1708_04233_b200 as W
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    p = W.Params.from_config(cfg)
+    pts = make_points(cfg)
+    n = len(pts)
+    d_pts = torch.from_numpy(pts).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        tot = 0.0
+        for _ in range(steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            tot += e0.elapsed_time(e1)
+        return tot / steps
+
+    pl = W.Pipeline(p, n, 0, p.n_h, device=dev, want_u=False)
+    t_w = timed(lambda: pl.run(d_pts), args.steps, args.warmup)
+    del pl
+    torch.cuda.empty_cache()
+    tb, sb = W.psf_tables_bytes(p)
+    tables = torch.empty(tb, dtype=torch.uint8, device=dev)
+    scr = torch.empty(sb, dtype=torch.uint8, device=dev)
+    W.build_psf_tables(p, tables, scr)                 # descriptors only (untimed): geometry of every depth
+    del scr
+    dense = torch.empty(W.psf_dense_bytes(p), dtype=torch.uint8, device=dev)
+    bins = torch.empty(W.bin_points_bytes(p, n, 0, p.n_h), dtype=torch.uint8, device=dev)
+    u = torch.empty((p.n_h, p.n_h, 2), dtype=torch.float32, device=dev)
+    bits = torch.empty((p.n_h, p.n_h // 8), dtype=torch.uint8, device=dev)
+    pr = W.PrintParams()
+    stage = {}
+
+    def direct_step():
+        W.build_psf_dense(p, dense)
+        W.bin_points_psf(p, tables, d_pts, 0, p.n_h, bins)
+        W.direct_sum(p, dense, bins, 0, p.n_h, u)
+        W.quantize(p, pr, u, 0, p.n_h, bits)
+
+    clocks = Clocks(0, os.path.join(ROOT, "gpurun_out", "clocks_direct.csv")
+                    if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp/clocks_direct.csv")
+    clocks.start()
+    t_d = timed(direct_step, max(1, args.steps // 2), 1)
+    ck = clocks.stop()
+    st = W.bins_stats(bins)
+    px = cfg.n_h * cfg.n_h
+    out = {"metric": METRIC, "value": px / (t_d * 1e-3) / 1e9, "unit": UNIT, "n_gpus": 1, "impl": "direct_sum",
+           "steps": max(1, args.steps // 2), "warmup": 1, "ms_per_step": t_d, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded generators, inputs/)",
+           "config": {"workload": _workload(cfg), "path": "conventional: dense PSF + disc bins + stamping "
+                      "(quantised direct sum of Eq.(1)) + quantise", "n_h": cfg.n_h, "n_points": n},
+           "wasabi_ms_per_step": t_w, "wasabi_speedup_vs_direct": t_d / t_w, "direct_bin_entries": st["entries"],
+           "clocks": ck,
+           "paper_context": {"wasabi_vs_conventional_cpu": "~30x (PAPER.md:164-167; 354 s vs 10,533 s N-LUT)"}}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -483,6 +562,8 @@ def main():
     ap.add_argument("--unfused", action="store_true", help="time the 4-call path (psi through HBM)")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo (test mode)")
     ap.add_argument("--same-device", action="store_true", help="test mode: all ranks on cuda:0")
+    ap.add_argument("--direct", action="store_true",
+                    help="time the conventional method (GPU direct sum) against WASABI on one GPU")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.points:
@@ -493,6 +574,8 @@ def main():
         cfg = cfg.replace(tile=args.tile)
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.direct:
+        run_direct(args, cfg)
     else:
         run_ours(args, cfg)
 

@@ -199,7 +199,15 @@ wasabi_status wasabi_quantize(const wasabi_params *params, const wasabi_print_pa
  * Dense tables: one (2H_d)^2 complex64 table per depth (caller-owned buffer). */
 wasabi_status wasabi_psf_dense_bytes(const wasabi_params *params, size_t *bytes);
 wasabi_status wasabi_build_psf_dense(const wasabi_params *params, void *d_dense, size_t bytes, cudaStream_t stream);
-/* d_bins from wasabi_bin_points for the same band; d_u: (row1 - row0) x n_h complex64, overwritten. */
+/* Bins for the direct sum: as wasabi_bin_points, but a point is listed in every tile its whole PSF disc
+ * (R-A2: ceil(R) per axis, squared distance ceil(R^2)) reaches, not only the tiles its kept coefficients
+ * reach (R-A19) -- the conventional method stamps the unshrunk PSF.  Standard parameters only (no
+ * EXACT_SHIFT / COIFLET: EINVAL).  Same buffer size query (wasabi_bin_points_bytes). */
+wasabi_status wasabi_bin_points_psf(const wasabi_params *params, const void *d_tables, const float *d_points,
+                                    int64_t n, int64_t row0, int64_t row1, void *d_bins, size_t bin_bytes,
+                                    cudaStream_t stream);
+/* d_bins from wasabi_bin_points_psf (or wasabi_bin_points: then only the kept coefficients' reach is
+ * covered) for the same band; d_u: (row1 - row0) x n_h complex64, overwritten. */
 wasabi_status wasabi_direct_sum(const wasabi_params *params, const void *d_dense, const void *d_bins, int64_t row0,
                                 int64_t row1, float *d_u, cudaStream_t stream);
 

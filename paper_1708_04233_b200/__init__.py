@@ -113,6 +113,7 @@ def lib() -> C.CDLL:
             "wasabi_table_count": [_PP, C.POINTER(_i64)],
             "wasabi_bin_points_bytes": [_PP, _i64, _i64, _i64, C.POINTER(_sz)],
             "wasabi_bin_points": [_PP, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp],
+            "wasabi_bin_points_psf": [_PP, _vp, _vp, _i64, _i64, _i64, _vp, _sz, _vp],
             "wasabi_superpose": [_PP, _vp, _vp, _i64, _i64, _vp, _vp],
             "wasabi_superpose_inverse": [_PP, _vp, _vp, _i64, _i64, _PR, _vp, _vp, _vp],
             "wasabi_inverse_wt": [_PP, _vp, _vp, _i64, _i64, _PR, _vp, _vp],
@@ -246,6 +247,12 @@ def psf_dense_bytes(p: Params) -> int:
 
 def build_psf_dense(p: Params, dense, stream=None):
     _check(lib().wasabi_build_psf_dense(C.byref(p.c()), _ptr(dense), _nbytes(dense), _stream(stream)))
+
+
+def bin_points_psf(p: Params, tables, points, row0: int, row1: int, bins, stream=None):
+    """Bins by the whole PSF disc (the direct sum's footprint)."""
+    _check(lib().wasabi_bin_points_psf(C.byref(p.c()), _ptr(tables), _ptr(points), points.shape[0], row0, row1,
+                                       _ptr(bins), _nbytes(bins), _stream(stream)))
 
 
 def direct_sum(p: Params, dense, bins, row0: int, row1: int, u, stream=None):

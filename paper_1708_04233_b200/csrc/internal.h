@@ -18,7 +18,7 @@ __host__ __device__ inline uint32_t pack_entry_pos(int X, int Y, int level) {
     return (uint32_t)X | ((uint32_t)Y << 14) | ((uint32_t)level << 28);
 }
 
-// Compact per-table data read by the hot kernels (72 bytes).
+// Compact per-table data read by the hot kernels (80 bytes).
 struct KDesc {
     int32_t H;                    // table half side (H, vbase: one 8-byte load in the hot kernel)
     int32_t vbase;                // window LUT pointer slots of this table start here (== vptr_base[0])
@@ -28,6 +28,8 @@ struct KDesc {
     int32_t ptr_base[kMaxLevels]; // canonical LUT: level l (1..L) band pointer rows start at ptr_base[l-1]
     int32_t vptr_base[kMaxLevels];// window LUT: level l pointer rows start at vptr_base[l-1]
     int32_t side;                 // table side: 2H, or 2H + 2^L for offset-class tables (R-A20)
+    int32_t Ed;                   // PSF-disc reach per axis, ceil(R) (bins of the direct sum)
+    int32_t Qd;                   // PSF-disc reach, squared distance ceil(R^2)
 };
 static_assert(sizeof(KDesc) % 8 == 0, "KDesc: (H, vbase) is read as one 8-byte load");
 
@@ -161,9 +163,10 @@ cudaError_t launch_scan_u32_to_u64(const uint32_t *in, unsigned long long *out, 
                                    cudaStream_t s);
 size_t scan_scratch_bytes(int64_t n);
 
+// psf = 1: bins by the whole PSF disc (Ed, Qd) instead of the kept coefficients' reach (direct sum)
 cudaError_t launch_bin(const BinHeader &bh, void *d_bins, const KDesc *kd, const float4 *pts,
                        double pitch, int64_t n_h, double z_min, double dz, int n_depth, int cls_bits,
-                       cudaStream_t s);
+                       int psf, cudaStream_t s);
 
 // Eq.(2) accumulation count of band [row0, row1) into *d_count (device u64) and, if d_row_work !=
 // NULL (n_h + 1 doubles), the per-row work estimate of the balanced bands (inclusive prefix sums of

@@ -22,6 +22,7 @@ struct BinArgs {
     int64_t n;
     int64_t n_h, row0, row1;
     int T, tiles_x, tiles_y, n_depth, cls_bits;
+    int psf;              // 1: footprint = the whole PSF disc (Ed, Qd; bins of the direct sum)
     double pitch, z_min, dz;
 };
 
@@ -76,9 +77,9 @@ __device__ __forceinline__ void warp_footprint(int4 q, bool valid, const KDesc *
         const int ix = __shfl_sync(0xffffffffu, q.x, src), iy = __shfl_sync(0xffffffffu, q.y, src);
         const int iz = __shfl_sync(0xffffffffu, q.z, src);
         const int tb = table_of(ix, iy, iz, A.cls_bits);
-        const int Q = __ldg(&kd[tb].Q);
+        const int Q = A.psf ? __ldg(&kd[tb].Qd) : __ldg(&kd[tb].Q);
         int tx0, tx1, ty0, ty1;
-        tile_range(ix, iy, __ldg(&kd[tb].Ek), A, tx0, tx1, ty0, ty1);
+        tile_range(ix, iy, A.psf ? __ldg(&kd[tb].Ed) : __ldg(&kd[tb].Ek), A, tx0, tx1, ty0, ty1);
         const int w = tx1 - tx0 + 1, hgt = ty1 - ty0 + 1;
         if (w <= 0 || hgt <= 0) continue;              // footprint entirely outside the band
         const int nbox = w * hgt;
@@ -341,7 +342,7 @@ cudaError_t launch_count_acc(const TableHeader &h, const void *d_tables, const f
     cudaError_t e;
     BinArgs A;
     A.n = n; A.n_h = n_h; A.row0 = row0; A.row1 = row1;
-    A.T = h.tile; A.tiles_x = 0; A.tiles_y = 0; A.n_depth = n_depth; A.cls_bits = cls_bits;
+    A.T = h.tile; A.tiles_x = 0; A.tiles_y = 0; A.n_depth = n_depth; A.cls_bits = cls_bits; A.psf = 0;
     A.pitch = pitch; A.z_min = z_min; A.dz = dz;
     if ((e = cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
     if (d_row_work && (e = cudaMemsetAsync(d_row_work, 0, sizeof(double) * (size_t)(n_h + 1), s)) != cudaSuccess)
@@ -361,7 +362,7 @@ cudaError_t launch_count_acc(const TableHeader &h, const void *d_tables, const f
 }
 
 cudaError_t launch_bin(const BinHeader &h, void *d_bins, const KDesc *kd, const float4 *pts, double pitch,
-                       int64_t n_h, double z_min, double dz, int n_depth, int cls_bits, cudaStream_t s) {
+                       int64_t n_h, double z_min, double dz, int n_depth, int cls_bits, int psf, cudaStream_t s) {
     char *base = reinterpret_cast<char *>(d_bins);
     BinHeader *bh = reinterpret_cast<BinHeader *>(base);
     int4 *pconv = reinterpret_cast<int4 *>(base + h.pts_off);
@@ -377,6 +378,7 @@ cudaError_t launch_bin(const BinHeader &h, void *d_bins, const KDesc *kd, const 
     BinArgs A;
     A.n = h.n_points; A.n_h = n_h; A.row0 = h.row0; A.row1 = h.row1;
     A.T = h.T; A.tiles_x = h.tiles_x; A.tiles_y = h.tiles_y; A.n_depth = n_depth; A.cls_bits = cls_bits;
+    A.psf = psf;
     A.pitch = pitch; A.z_min = z_min; A.dz = dz;
     cudaError_t e;
     if ((e = cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(h.n_tiles + 1), s)) != cudaSuccess) return e;

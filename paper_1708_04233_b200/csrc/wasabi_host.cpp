@@ -221,6 +221,9 @@ wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
         coef += side * side;
         K.H = (int32_t)H;
         K.E = (int32_t)E;
+        K.Ed = (int32_t)std::ceil(R);
+        K.Qd = (int32_t)std::ceil(R * R);
+
         g.max_E = std::max(g.max_E, E);
         D.group_base = (int32_t)ptr;
         for (int l = 1; l <= g.L; l++) {
@@ -473,8 +476,10 @@ wasabi_status wasabi_bin_points_bytes(const wasabi_params *params, int64_t n, in
     return WASABI_OK;
 }
 
-wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_tables, const float *d_points, int64_t n,
-                                int64_t row0, int64_t row1, void *d_bins, size_t bin_bytes, cudaStream_t stream) {
+namespace {
+wasabi_status bin_points_impl(const wasabi_params *params, const void *d_tables, const float *d_points, int64_t n,
+                              int64_t row0, int64_t row1, void *d_bins, size_t bin_bytes, int psf,
+                              cudaStream_t stream) {
     Geo g;
     wasabi_status st = compute_geo(params, g);
     if (st != WASABI_OK) return st;
@@ -488,9 +493,23 @@ wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_table
     CK(launch_write_blob(d_bins, &b.h, sizeof b.h, stream), "write bin header");
     const KDesc *kd = reinterpret_cast<const KDesc *>(static_cast<const char *>(d_tables) + g.th.kdesc_off);
     CK(launch_bin(b.h, d_bins, kd, reinterpret_cast<const float4 *>(d_points), params->pitch_m, params->n_h,
-                  params->z_min_m, g.dz, g.nz, g.cb, stream),
+                  params->z_min_m, g.dz, g.nz, g.cb, psf, stream),
        "bin");
     return WASABI_OK;
+}
+}  // namespace
+
+wasabi_status wasabi_bin_points(const wasabi_params *params, const void *d_tables, const float *d_points, int64_t n,
+                                int64_t row0, int64_t row1, void *d_bins, size_t bin_bytes, cudaStream_t stream) {
+    return bin_points_impl(params, d_tables, d_points, n, row0, row1, d_bins, bin_bytes, 0, stream);
+}
+
+wasabi_status wasabi_bin_points_psf(const wasabi_params *params, const void *d_tables, const float *d_points,
+                                    int64_t n, int64_t row0, int64_t row1, void *d_bins, size_t bin_bytes,
+                                    cudaStream_t stream) {
+    if (params && (params->flags & (WASABI_FLAG_EXACT_SHIFT | WASABI_FLAG_COIFLET)))
+        return fail(WASABI_EINVAL, "wasabi_bin_points_psf: standard (one table per depth) parameters only");
+    return bin_points_impl(params, d_tables, d_points, n, row0, row1, d_bins, bin_bytes, 1, stream);
 }
 
 wasabi_status wasabi_count_accumulations(const wasabi_params *params, const void *d_tables, const float *d_points,

@@ -445,7 +445,7 @@ def _direct_gpu(W, cfg, pts, row0, row1):
     pl = W.Pipeline(p, max(1, len(pts)), row0, row1)
     d = torch.from_numpy(np.ascontiguousarray(pts)).cuda()
     pl.build_tables()
-    pl.bin(d)
+    W.bin_points_psf(p, pl.tables, d, row0, row1, pl.bins)      # the whole PSF disc (conventional method)
     dense = torch.empty(W.psf_dense_bytes(p), dtype=torch.uint8, device="cuda")
     W.build_psf_dense(p, dense)
     u = torch.empty((row1 - row0, p.n_h, 2), dtype=torch.float32, device="cuda")
@@ -539,3 +539,25 @@ def test_count_accumulations_equals_oracle(W, orc, name, n, row0, row1, kw):
     W.row_work(p, t, d, rw, s8)
     full = W.count_accumulations(p, t, d, 0, cfg.n_h, s8)
     assert abs(float(rw[:cfg.n_h].sum()) - full) <= 1e-6 * full
+
+
+def test_psf_bins_contain_reach_bins(W):
+    """Bins by the PSF disc (wasabi_bin_points_psf) list, per tile, a superset of the reach bins
+    (R-A19: the kept coefficients of a depth lie inside its PSF's Haar blocks), in ascending order."""
+    import torch
+    cfg = CONFIGS["C2"]
+    pts = make_points(cfg, n=3000)
+    p = gpu_params(cfg)
+    t = _tables(W, p)
+    d = torch.from_numpy(pts).cuda()
+    b1 = torch.empty(W.bin_points_bytes(p, len(pts), 0, 2048), dtype=torch.uint8, device="cuda")
+    b2 = torch.empty_like(b1)
+    W.bin_points(p, t, d, 0, 2048, b1)
+    W.bin_points_psf(p, t, d, 0, 2048, b2)
+    torch.cuda.synchronize()
+    p1, i1 = W.export_bins(p, b1)
+    p2, i2 = W.export_bins(p, b2)
+    for k in range(len(p1) - 1):
+        a, b = i1[p1[k]:p1[k + 1]], i2[p2[k]:p2[k + 1]]
+        assert np.all(np.diff(b) > 0)
+        assert np.all(np.isin(a, b))
