@@ -211,6 +211,18 @@ wasabi_status wasabi_bin_points_psf(const wasabi_params *params, const void *d_t
 wasabi_status wasabi_direct_sum(const wasabi_params *params, const void *d_dense, const void *d_bins, int64_t row0,
                                 int64_t row1, float *d_u, cudaStream_t stream);
 
+/* The EXACT Eq.(1) on the GPU -- "D1": u(X, Y) = sum_j a_j exp(i k r_j) with the continuous
+ * (x_j, y_j, z_j) (no position or depth quantisation), r_j = sqrt((x - x_j)^2 + (y - y_j)^2 + z_j^2), over
+ * the diffraction-limited window rho < |z_j| tan(asin(lambda/2p)) (+ the rho = 0 pixel; R-A2 at the
+ * point's own depth).  The window test and r_j in fp64 (the oracle's operation sequence), the phase as the
+ * fp64 quarter-cycle count 4 r_j / lambda with (cos, sin) of its fraction in fp32 (< 1e-7), fp32
+ * accumulation in point order.  The PSNR reference of the C5 sweep (R-A18).  d_points: the original
+ * n x 4 float32 points; d_bins from wasabi_bin_points_psf for the same band and points (its reach
+ * covers a point anywhere within half a depth level of its level, i.e. every point the bins accept;
+ * points the bins skip -- R-A17 -- do not contribute).  d_u: (row1 - row0) x n_h complex64, overwritten. */
+wasabi_status wasabi_direct_exact(const wasabi_params *params, const float *d_points, int64_t n, const void *d_bins,
+                                  int64_t row0, int64_t row1, float *d_u, cudaStream_t stream);
+
 /* ---------------------------------------------------------------- work accounting (not the hot path) */
 
 /* The exact number of Eq.(2) accumulations whose target lies in the hologram

@@ -123,6 +123,7 @@ def lib() -> C.CDLL:
             "wasabi_psf_dense_bytes": [_PP, C.POINTER(_sz)],
             "wasabi_build_psf_dense": [_PP, _vp, _sz, _vp],
             "wasabi_direct_sum": [_PP, _vp, _vp, _i64, _i64, _vp, _vp],
+            "wasabi_direct_exact": [_PP, _vp, _i64, _vp, _i64, _i64, _vp, _vp],
             "wasabi_tables_check": [_PP, _vp],
             "wasabi_export_table": [_PP, _vp, C.c_int32, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
             "wasabi_export_bins": [_PP, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
@@ -273,6 +274,12 @@ def row_work(p: Params, tables, points, out, scratch, stream=None):
     """Per-row work estimate into `out` (n_h + 1 float64 device tensor; out[:n_h] meaningful)."""
     _check(lib().wasabi_row_work(C.byref(p.c()), _ptr(tables), _ptr(points), points.shape[0], _ptr(out),
                                  _ptr(scratch), _stream(stream)))
+
+
+def direct_exact(p: Params, points, bins, row0: int, row1: int, u, stream=None):
+    """Exact Eq.(1) (D1: continuous positions and depths) for a band; bins from bin_points_psf."""
+    _check(lib().wasabi_direct_exact(C.byref(p.c()), _ptr(points), points.shape[0], _ptr(bins), row0, row1,
+                                     _ptr(u), _stream(stream)))
 
 
 # ----------------------------------------------------------------------------- whole path

@@ -28,8 +28,8 @@ struct KDesc {
     int32_t ptr_base[kMaxLevels]; // canonical LUT: level l (1..L) band pointer rows start at ptr_base[l-1]
     int32_t vptr_base[kMaxLevels];// window LUT: level l pointer rows start at vptr_base[l-1]
     int32_t side;                 // table side: 2H, or 2H + 2^L for offset-class tables (R-A20)
-    int32_t Ed;                   // PSF-disc reach per axis, ceil(R) (bins of the direct sum)
-    int32_t Qd;                   // PSF-disc reach, squared distance ceil(R^2)
+    int32_t Ed;                   // PSF-disc reach per axis, ceil(Rh), Rh = R(|z_d| + dz/2) + 1 (direct sums)
+    int32_t Qd;                   // PSF-disc reach, squared distance ceil(Rh^2)
 };
 static_assert(sizeof(KDesc) % 8 == 0, "KDesc: (H, vbase) is read as one 8-byte load");
 
@@ -187,6 +187,10 @@ cudaError_t launch_psf_dense(const DenseDesc *d_desc, int n_depth, float2 *out, 
                              int64_t total_ctas, cudaStream_t s);
 cudaError_t launch_stamp(const void *d_bins, const DenseDesc *d_desc, const float2 *dense, int tiles_x, int tiles_y,
                          int64_t row0, int64_t n_h, int T, float2 *u, cudaStream_t s);
+
+// exact Eq.(1) (D1) of a band from the original points and PSF-disc bins
+cudaError_t launch_exact(const void *d_bins, const float4 *pts, int tiles_x, int tiles_y, int64_t row0, int64_t n_h,
+                         int T, double pitch, double tan_theta, double wavelength, float2 *u, cudaStream_t s);
 
 cudaError_t launch_inverse(const float2 *psi, float2 *u, int64_t rows, int64_t n_h, int64_t row0, int levels,
                            const double *print4 /* xr, yr, zr, inv_lambda or NULL */, double pitch,

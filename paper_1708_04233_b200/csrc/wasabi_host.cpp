@@ -221,8 +221,12 @@ wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
         coef += side * side;
         K.H = (int32_t)H;
         K.E = (int32_t)E;
-        K.Ed = (int32_t)std::ceil(R);
-        K.Qd = (int32_t)std::ceil(R * R);
+        {   // PSF-disc reach: the level's disc (D2) and the continuous point's (D1: |z| within half a level
+            // of z_d, pixel rounding +-1/2 px), so both direct sums find every contributing point
+            const double Rh = (std::fabs(z) + 0.5 * g.dz) * g.tan_theta / P->pitch_m + 1.0;
+            K.Ed = (int32_t)std::ceil(Rh);
+            K.Qd = (int32_t)std::ceil(Rh * Rh);
+        }
 
         g.max_E = std::max(g.max_E, E);
         D.group_base = (int32_t)ptr;
@@ -698,6 +702,22 @@ wasabi_status wasabi_direct_sum(const wasabi_params *params, const void *d_dense
                     (int)(params->n_h / T), (int)((row1 - row0) / T), row0, params->n_h, T,
                     reinterpret_cast<float2 *>(d_u), stream),
        "direct_sum");
+    return WASABI_OK;
+}
+
+wasabi_status wasabi_direct_exact(const wasabi_params *params, const float *d_points, int64_t n, const void *d_bins,
+                                  int64_t row0, int64_t row1, float *d_u, cudaStream_t stream) {
+    Geo g;
+    wasabi_status st = compute_geo(params, g);
+    if (st != WASABI_OK) return st;
+    if ((st = validate_band(params, row0, row1)) != WASABI_OK) return st;
+    if (!d_bins || (!d_u && row1 > row0) || (n > 0 && !d_points)) return fail(WASABI_EINVAL, "NULL buffer");
+    if (n > 0 && !aligned(d_points, 16)) return fail(WASABI_EINVAL, "d_points must be 16-byte aligned");
+    const int T = params->tile;
+    CK(launch_exact(d_bins, reinterpret_cast<const float4 *>(d_points), (int)(params->n_h / T), (int)((row1 - row0) / T),
+                    row0, params->n_h, T, params->pitch_m, g.tan_theta, params->wavelength_m,
+                    reinterpret_cast<float2 *>(d_u), stream),
+       "direct_exact");
     return WASABI_OK;
 }
 

@@ -561,3 +561,30 @@ def test_psf_bins_contain_reach_bins(W):
         a, b = i1[p1[k]:p1[k + 1]], i2[p2[k]:p2[k + 1]]
         assert np.all(np.diff(b) > 0)
         assert np.all(np.isin(a, b))
+
+
+# ---------------------------------------------------------------- exact Eq.(1) (D1) on the GPU
+@pytest.mark.parametrize("name,n,row0,row1,x0,w", [("C1", None, 0, 512, 0, 512), ("C2", 1500, 512, 768, 0, 2048),
+                                                  ("C5", 10_000, 8192, 8256, 7680, 512),
+                                                  ("C4", 200_000, 32768, 32832, 32768, 256)])
+def test_direct_exact_equals_oracle_d1(W, orc, name, n, row0, row1, x0, w):
+    """wasabi_direct_exact (continuous x, y, z) == the oracle's D1 on the same points,
+    element-wise within 1e-5 of max|u| and in rel L2 (fp64 window test and distance, fp32 phase split)."""
+    import torch
+    cfg = CONFIGS[name]
+    pts = make_points(cfg, n=n)
+    p = gpu_params(cfg)
+    t = _tables(W, p)
+    d = torch.from_numpy(pts).cuda()
+    bins = torch.empty(W.bin_points_bytes(p, len(pts), row0, row1), dtype=torch.uint8, device="cuda")
+    W.bin_points_psf(p, t, d, row0, row1, bins)
+    u = torch.empty((row1 - row0, p.n_h, 2), dtype=torch.float32, device="cuda")
+    W.direct_exact(p, d, bins, row0, row1, u)
+    torch.cuda.synchronize()
+    P = orc_params(orc, cfg)
+    sel = np.abs(pts[:, 1] / cfg.pitch + cfg.n_h // 2 - (row0 + row1) / 2) < (row1 - row0) / 2 + 800
+    d1 = orc.direct_d1(P, pts[sel].astype(np.float64), x0, row0, w, row1 - row0)
+    e, m = field_check(field_np(u)[:, x0:x0 + w], d1)
+    parity_log(dict(case=f"D1 {name} rows [{row0},{row1}) x [{x0},{x0 + w})", rel_u=e, max_u=m))
+    assert np.linalg.norm(d1) > 0
+    assert e <= 1e-5 and m <= 1e-5, (e, m)
