@@ -66,8 +66,8 @@ typedef struct {
     double retention;     /* r in (0, 1]: N_r,d = min(nnz_d, ceil(r_ppm nnz_d / 1e6)), r_ppm =
                              llround(r 1e6) >= 1 (R-A4; the paper's N_r = pi (W/2)^2 gamma, :92)   */
     int32_t tile;         /* T: bin / superposition tile side; 64 or 128 (multiple of 2^L)        */
-    uint32_t flags;       /* 0, WASABI_FLAG_EXACT_SHIFT or WASABI_FLAG_COIFLET (not both);
-                             other bits: EINVAL                                                    */
+    uint32_t flags;       /* 0, WASABI_FLAG_EXACT_SHIFT or WASABI_FLAG_COIFLET (not both), optionally
+                             | WASABI_FLAG_GATHER or WASABI_FLAG_SCATTER; other bits: EINVAL       */
 } wasabi_params;
 
 /* Exact off-grid shifts (reading R-A20; needs levels <= 4).  Instead of
@@ -90,6 +90,17 @@ typedef struct {
  * then wasabi_inverse_wt (d_psi = that halo band, transformed in place).  wasabi_superpose_inverse
  * (the fused Haar kernel) returns EINVAL in this mode; wasabi_hologram_host handles it. */
 #define WASABI_FLAG_COIFLET 2u
+
+/* Dense gather superposition (the r -> 100% regime).  Eq.(2) is a sum of
+ * sparse kept coefficients; at high retention the kept set is nearly dense and a per-pixel GATHER from
+ * a dense wavelet-domain table (kept value or 0; one (side x side) complex64 table per PSF table) beats
+ * the scatter of the kept list.  Each pixel of level l (R-A6) reads table(X - s_l(ix) + H, Y - s_l(iy)
+ * + H) for every point of its tile's bin, in bin order: unkept coefficients add an exact 0, so psi is
+ * BIT-IDENTICAL to the scatter path.  Default (neither flag): gather iff retention >= 0.6, tile == 64,
+ * levels >= 2 and not coiflets; the flags force one path (GATHER needs tile 64, levels >= 2, Haar).
+ * In gather mode the table buffer holds the dense tables instead of the superposition's window LUT. */
+#define WASABI_FLAG_GATHER 4u
+#define WASABI_FLAG_SCATTER 8u
 
 /* Rows of psi halo the coiflet inverse needs on each side of a band (= tile; 0 for Haar). */
 int64_t wasabi_coif_halo_rows(const wasabi_params *params);

@@ -19,6 +19,8 @@ WASABI_OK, WASABI_EINVAL, WASABI_ENOSPC, WASABI_ECUDA, WASABI_ESTATE = 0, -1, -2
 
 FLAG_EXACT_SHIFT = 1   # include/wasabi.h WASABI_FLAG_EXACT_SHIFT
 FLAG_COIFLET = 2       # include/wasabi.h WASABI_FLAG_COIFLET
+FLAG_GATHER = 4        # include/wasabi.h WASABI_FLAG_GATHER (dense gather superposition)
+FLAG_SCATTER = 8       # include/wasabi.h WASABI_FLAG_SCATTER (window-LUT scatter superposition)
 
 
 class WasabiError(RuntimeError):
@@ -57,6 +59,7 @@ class Params:
     tile: int = 64
     exact: bool = False   # WASABI_FLAG_EXACT_SHIFT: offset-class tables (R-A20)
     wavelet: int = 0      # 0 Haar; 1 WASABI_FLAG_COIFLET: coif1, the paper's coiflets (R-A21, NEXT-2)
+    path: str = "auto"    # superposition: "auto" (gather iff r >= 0.6), "gather" or "scatter" (wasabi.h)
 
     @staticmethod
     def from_config(cfg, **kw) -> "Params":
@@ -67,7 +70,8 @@ class Params:
     def c(self) -> _CParams:
         return _CParams(self.wavelength, self.pitch, self.n_h, self.n_depth, self.levels, self.z_min,
                         self.z_max, self.retention, self.tile,
-                        (FLAG_EXACT_SHIFT if self.exact else 0) | (FLAG_COIFLET if self.wavelet == 1 else 0))
+                        (FLAG_EXACT_SHIFT if self.exact else 0) | (FLAG_COIFLET if self.wavelet == 1 else 0)
+                        | {"auto": 0, "gather": FLAG_GATHER, "scatter": FLAG_SCATTER}[self.path])
 
     def halo_rows(self) -> int:
         """psi rows the inverse needs beyond a band on each side (wasabi_coif_halo_rows)."""

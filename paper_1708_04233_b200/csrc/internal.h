@@ -74,6 +74,29 @@ __host__ __device__ inline int win_slots(int side, int l, int cb) {
     return win_variants(l, cb) * win_bands(side) * (win_cols(side, l) + 1);
 }
 
+// Dense wavelet tables of the gather superposition (WASABI_FLAG_GATHER), Mallat (subband-planar)
+// order: table side s, s_l = s >> l; level l = 1..L, subband b = 0 (X & h, Y even at h), 1 (Y & h
+// only), 2 (both), h = 2^(l-1), is the s_l x s_l plane at mallat_plane(s, l) + b s_l^2, cell (X >> l,
+// Y >> l) row-major; LL (X, Y multiples of 2^L) is the plane at mallat_plane(s, L + 1).  A level-l
+// shift by a multiple of 2^l (R-A8, R-A20) is then an integer translation of the level's planes.
+__host__ __device__ inline int32_t mallat_plane(int s, int l) {
+    int32_t off = 0;
+    for (int k = 1; k < l; k++) off += 3 * (s >> k) * (s >> k);
+    return off;
+}
+__host__ __device__ inline int64_t mallat_index(int X, int Y, int s, int L) {
+    const int m = X | Y;
+    for (int l = 1; l <= L; l++) {
+        const int h = 1 << (l - 1);
+        if (m & h) {
+            const int sl = s >> l, b = ((Y & h) ? 1 : 0) + (((X & h) && (Y & h)) ? 1 : 0);
+            return (int64_t)mallat_plane(s, l) + (int64_t)b * sl * sl + (int64_t)(Y >> l) * sl + (X >> l);
+        }
+    }
+    const int sL = s >> L;
+    return (int64_t)mallat_plane(s, L + 1) + (int64_t)(Y >> L) * sL + (X >> L);
+}
+
 // Per-depth data used by the table build and exports.
 struct DDesc {
     double z, R;
@@ -102,8 +125,8 @@ struct TableHeader {
     int64_t vent_cap;                  // window-LUT entry capacity (bound: 16 N_r per depth)
     int64_t vptr_off, vval_off, vpos_off;  // window LUT: pointers, float2 values, uint16 positions
     int32_t cls_bits, n_zlevels;       // offset-class bits cb (0 or L) and depth levels N_z
-    int32_t wavelet, pad1;             // 0 Haar, 1 coif1 (R-A21)
-    int64_t pad[1];
+    int32_t wavelet, gather;           // 0 Haar, 1 coif1 (R-A21); 1: dense gather superposition
+    int64_t dense_off;                 // dense wavelet tables (gather mode), byte offset
 };
 static_assert(sizeof(TableHeader) <= 256, "table header must fit the 256-byte slot");
 
@@ -158,6 +181,8 @@ cudaError_t launch_coif_tables(const TableHeader &h, const void *d_tables, doubl
                                int64_t n_coef, double k, double pitch, int L, cudaStream_t s);
 // coif1 synthesis of a psi band (nrows x n_h) in place, levels L..1
 cudaError_t launch_coif_inverse(float2 *psi, int64_t nrows, int64_t n_h, int L, cudaStream_t s);
+// gather mode: every kept canonical entry written into its table's dense copy (zeroed beforehand)
+cudaError_t launch_dense_fill(const TableHeader &h, void *d_tables, cudaStream_t s);
 cudaError_t launch_scan_i32(int32_t *data, int64_t n, void *scratch, cudaStream_t s);
 cudaError_t launch_scan_u32_to_u64(const uint32_t *in, unsigned long long *out, int64_t n, void *scratch,
                                    cudaStream_t s);
@@ -181,6 +206,10 @@ cudaError_t launch_count_acc(const TableHeader &h, const void *d_tables, const f
 cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int cls_bits, int tiles_x,
                              int tiles_y, int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4,
                              double pitch, uint8_t *bits, cudaStream_t s, int tile_row0 = 0, int tile_row1 = -1);
+// dense gather superposition (gather-mode tables, T = 64): same outputs as launch_superpose
+cudaError_t launch_gather(const void *d_bins, const void *d_tables, int L, int cls_bits, int tiles_x, int tiles_y,
+                          int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
+                          uint8_t *bits, cudaStream_t s, int tile_row0 = 0, int tile_row1 = -1);
 cudaError_t launch_write_blob(void *dst, const void *src, size_t bytes, cudaStream_t s);
 
 cudaError_t launch_psf_dense(const DenseDesc *d_desc, int n_depth, float2 *out, double k, double pitch,

@@ -158,6 +158,82 @@ __device__ __forceinline__ int class_level(int c, int j, int L) {
     return l <= L ? l : 0;
 }
 
+// Steps 3 (+4) of a T x T psi tile held in shared memory (swizzled cells, swz), shared by the scatter
+// and gather superposition kernels: fused -> the R-A6 inverse butterflies level by level in place, the
+// print bits (print_byte) and u (psi pointer, may be NULL); unfused -> psi written as is.
+template <int T, int NT>
+__device__ __forceinline__ void tile_epilogue(float2 *tile, uint32_t tile_sa, int L, int fused, const QArgs &qa,
+                                              uint8_t *__restrict__ bits, float2 *__restrict__ psi, int64_t row0,
+                                              int64_t n_h, int tile_x0, int tile_y0) {
+    constexpr int M = kWinMargin, S = T + M;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    auto cell = [&](int r, int x) -> float2 & {
+        return tile[(swz(tile_sa + 8u * (uint32_t)(M + r * S + x)) - tile_sa) >> 3];
+    };
+    if (fused) {
+        // steps 3 (+4) in place: psi never leaves shared memory (SURVEY.md §8(f) NEXT-1); the
+        // R-A6 butterflies level by level from L (inv_butterfly, device_common.cuh), swizzled cells
+        for (int l = L; l >= 1; l--) {
+            const int st = 1 << (l - 1), nq = T >> l;
+#if WASABI_L1Q
+            if (l == 1) {   // a level-1 quad's rows are aligned 16-byte cell pairs (swapped for odd keys)
+                for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
+                    const int bx = (qd % nq) << 1, by = (qd / nq) << 1;
+                    const uint32_t a0 = swz(tile_sa + 8u * (uint32_t)(M + by * S + bx));
+                    const uint32_t a1 = swz(tile_sa + 8u * (uint32_t)(M + (by + 1) * S + bx));
+                    const float4 w0 = lds4(a0 & ~15u), w1 = lds4(a1 & ~15u);
+                    float2 q[4];
+                    q[0] = (a0 & 8u) ? make_float2(w0.z, w0.w) : make_float2(w0.x, w0.y);
+                    q[1] = (a0 & 8u) ? make_float2(w0.x, w0.y) : make_float2(w0.z, w0.w);
+                    q[2] = (a1 & 8u) ? make_float2(w1.z, w1.w) : make_float2(w1.x, w1.y);
+                    q[3] = (a1 & 8u) ? make_float2(w1.x, w1.y) : make_float2(w1.z, w1.w);
+                    inv_butterfly(&q[0], &q[1], &q[2], &q[3]);
+                    sts4(a0 & ~15u, (a0 & 8u) ? make_float4(q[1].x, q[1].y, q[0].x, q[0].y)
+                                              : make_float4(q[0].x, q[0].y, q[1].x, q[1].y));
+                    sts4(a1 & ~15u, (a1 & 8u) ? make_float4(q[3].x, q[3].y, q[2].x, q[2].y)
+                                              : make_float4(q[2].x, q[2].y, q[3].x, q[3].y));
+                }
+                __syncthreads();
+                continue;
+            }
+#endif
+            for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
+                const int bx = (qd % nq) << l, by = (qd / nq) << l;
+                inv_butterfly(&cell(by, bx), &cell(by, bx + st), &cell(by + st, bx), &cell(by + st, bx + st));
+            }
+            __syncthreads();
+        }
+        if (bits) {
+            constexpr int bpr = T / 8;
+            for (int bi = threadIdx.x; bi < T * bpr; bi += NT) {
+                const int row = bi / bpr, xb = bi % bpr;
+                const int64_t Y = tile_y0 + row;
+                float2 v[8];
+#pragma unroll
+                for (int i = 0; i < 8; i++) v[i] = cell(row, xb * 8 + i);
+                const unsigned byte = print_byte(v, tile_x0 + xb * 8, ref_row(Y, qa), qa);
+                bits[(Y - row0) * (n_h / 8) + tile_x0 / 8 + xb] = (uint8_t)byte;
+            }
+        }
+        if (!psi) return;
+    }
+    float2 *out = psi + (int64_t)(tile_y0 - row0) * n_h + tile_x0;
+#pragma unroll 4
+    for (int y = wid; y < T; y += NT / 32) {
+        float2 v[T / 32];                     // loads of a row first, then its coalesced stores
+#pragma unroll
+        for (int i = 0; i < T / 32; i++) v[i] = cell(y, lane + 32 * i);
+#pragma unroll
+        for (int i = 0; i < T / 32; i++) {
+#if WASABI_STCS   // write-once output: evict-first in L2, so it does not displace the window LUT
+            __stcs(out + (int64_t)y * n_h + lane + 32 * i, v[i]);
+#else
+            out[(int64_t)y * n_h + lane + 32 * i] = v[i];
+#endif
+        }
+    }
+}
+
 template <int T, bool EX>
 __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_kernel(const void *__restrict__ d_bins,
                                                                            const void *__restrict__ d_tables,
@@ -410,68 +486,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 #undef WASABI_PREFETCH
 #undef WASABI_CONSUME
     __syncthreads();
-    if (fused) {
-        // steps 3 (+4) in place: psi never leaves shared memory (SURVEY.md §8(f) NEXT-1); the
-        // R-A6 butterflies level by level from L (inv_butterfly, device_common.cuh), swizzled cells
-        for (int l = A.L; l >= 1; l--) {
-            const int st = 1 << (l - 1), nq = T >> l;
-#if WASABI_L1Q
-            if (l == 1) {   // a level-1 quad's rows are aligned 16-byte cell pairs (swapped for odd keys)
-                for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
-                    const int bx = (qd % nq) << 1, by = (qd / nq) << 1;
-                    const uint32_t a0 = swz(tile_sa + 8u * (uint32_t)(M + by * S + bx));
-                    const uint32_t a1 = swz(tile_sa + 8u * (uint32_t)(M + (by + 1) * S + bx));
-                    const float4 w0 = lds4(a0 & ~15u), w1 = lds4(a1 & ~15u);
-                    float2 q[4];
-                    q[0] = (a0 & 8u) ? make_float2(w0.z, w0.w) : make_float2(w0.x, w0.y);
-                    q[1] = (a0 & 8u) ? make_float2(w0.x, w0.y) : make_float2(w0.z, w0.w);
-                    q[2] = (a1 & 8u) ? make_float2(w1.z, w1.w) : make_float2(w1.x, w1.y);
-                    q[3] = (a1 & 8u) ? make_float2(w1.x, w1.y) : make_float2(w1.z, w1.w);
-                    inv_butterfly(&q[0], &q[1], &q[2], &q[3]);
-                    sts4(a0 & ~15u, (a0 & 8u) ? make_float4(q[1].x, q[1].y, q[0].x, q[0].y)
-                                              : make_float4(q[0].x, q[0].y, q[1].x, q[1].y));
-                    sts4(a1 & ~15u, (a1 & 8u) ? make_float4(q[3].x, q[3].y, q[2].x, q[2].y)
-                                              : make_float4(q[2].x, q[2].y, q[3].x, q[3].y));
-                }
-                __syncthreads();
-                continue;
-            }
-#endif
-            for (int qd = threadIdx.x; qd < nq * nq; qd += NT) {
-                const int bx = (qd % nq) << l, by = (qd / nq) << l;
-                inv_butterfly(&cell(by, bx), &cell(by, bx + st), &cell(by + st, bx), &cell(by + st, bx + st));
-            }
-            __syncthreads();
-        }
-        if (bits) {
-            constexpr int bpr = T / 8;
-            for (int bi = threadIdx.x; bi < T * bpr; bi += NT) {
-                const int row = bi / bpr, xb = bi % bpr;
-                const int64_t Y = tile_y0 + row;
-                float2 v[8];
-#pragma unroll
-                for (int i = 0; i < 8; i++) v[i] = cell(row, xb * 8 + i);
-                const unsigned byte = print_byte(v, tile_x0 + xb * 8, ref_row(Y, qa), qa);
-                bits[(Y - A.row0) * (A.n_h / 8) + tile_x0 / 8 + xb] = (uint8_t)byte;
-            }
-        }
-        if (!psi) return;
-    }
-    float2 *out = psi + (int64_t)(tile_y0 - A.row0) * A.n_h + tile_x0;
-#pragma unroll 4
-    for (int y = wid; y < T; y += NT / 32) {
-        float2 v[T / 32];                     // loads of a row first, then its coalesced stores
-#pragma unroll
-        for (int i = 0; i < T / 32; i++) v[i] = cell(y, lane + 32 * i);
-#pragma unroll
-        for (int i = 0; i < T / 32; i++) {
-#if WASABI_STCS   // write-once output: evict-first in L2, so it does not displace the window LUT
-            __stcs(out + (int64_t)y * A.n_h + lane + 32 * i, v[i]);
-#else
-            out[(int64_t)y * A.n_h + lane + 32 * i] = v[i];
-#endif
-        }
-    }
+    tile_epilogue<T, NT>(tile, tile_sa, A.L, fused, qa, bits, psi, A.row0, A.n_h, tile_x0, tile_y0);
 }
 
 template <int T, bool EX>
@@ -488,7 +503,217 @@ cudaError_t launch_t(const void *d_bins, const void *d_tables, const SupArgs &A,
     return cudaGetLastError();
 }
 
+// ---- dense gather superposition (gather-mode tables; wasabi.h WASABI_FLAG_GATHER) ----
+// Eq.(2) per PIXEL instead of per kept coefficient: a level-l pixel of the tile (R-A6) receives
+// a_j table_j(pixel - s_l + H_j) from every point j of the tile's bin, in bin order, from the point's
+// dense wavelet table (kept value or 0; R-A8 shifts, or the 2^L-aligned shift of the offset-class
+// tables, R-A20).  Unkept coefficients add an exact 0 and positions outside the table nothing, so psi
+// is bit-identical to the scatter kernel's.  The dense tables are in Mallat order (internal.h
+// mallat_index), where a level-l shift is an integer translation of the level's three subband planes:
+// in the tile's own Mallat view (level 1: 3 planes x 32 x 32 cells, level 2: 3 x 16 x 16, levels >= 3
+// and LL: 256 cells) every warp load is a contiguous run of one table plane row.  One CTA per 64 x 64
+// tile, 256 threads, psi in registers: thread (warp w, lane) owns 12 level-1 cells (plane b = k / 4,
+// plane row w + 8 (k % 4), column lane), 3 level-2 cells (plane k, row 2w + lane / 16, column lane % 16)
+// and one cell of levels >= 3 / LL (cell tid in level order); then psi goes to the shared tile in the
+// interleaved layout and through the scatter kernel's epilogue.
+struct GatherArgs {
+    int L, cls_bits, tiles_x, tile_rows;
+    int64_t row0, n_h, tile0;
+};
+struct GatherPoint {          // one point of a batch, per tile
+    const float2 *tp;         // its dense table
+    float a;
+    int s;                    // table side
+    int off[kMaxLevels + 1];  // Mallat plane-stack offset of level l (1..L), LL at [L]
+    int2 o[kMaxLevels];       // table plane coordinates of the tile's plane origin, per level
+    int in1;                  // the tile's level-1 window (32 x 32 per plane) lies inside the table
+    int pad;
+};
+constexpr int kGatherBatch = 64;
+
+__global__ void __launch_bounds__(256, 3) gather_kernel(const void *__restrict__ d_bins,
+                                                        const void *__restrict__ d_tables, GatherArgs A,
+                                                        float2 *__restrict__ psi, int fused, QArgs qa,
+                                                        uint8_t *__restrict__ bits) {
+    constexpr int T = 64, NT = 256;
+    extern __shared__ float2 tile[];
+    __shared__ GatherPoint gp[kGatherBatch];
+    const char *bb = reinterpret_cast<const char *>(d_bins);
+    const BinHeader *bh = reinterpret_cast<const BinHeader *>(bb);
+    const int4 *__restrict__ pconv = reinterpret_cast<const int4 *>(bb + bh->pts_off);
+    const unsigned long long *__restrict__ bptr = reinterpret_cast<const unsigned long long *>(bb + bh->ptr_off);
+    const uint32_t *__restrict__ bidx = reinterpret_cast<const uint32_t *>(bb + bh->idx_off);
+    const char *tb = reinterpret_cast<const char *>(d_tables);
+    const TableHeader *th = reinterpret_cast<const TableHeader *>(tb);
+    const KDesc *__restrict__ kd = reinterpret_cast<const KDesc *>(tb + th->kdesc_off);
+    const DDesc *__restrict__ dd = reinterpret_cast<const DDesc *>(tb + th->ddesc_off);
+    const float2 *__restrict__ dense = reinterpret_cast<const float2 *>(tb + th->dense_off);
+
+    int64_t t;
+    {   // the scatter kernel's tile order (groups of kGroup tile rows, column-major inside a group)
+        const int64_t per_group = (int64_t)kGroup * A.tiles_x;
+        const int64_t g = blockIdx.x / per_group, rem = blockIdx.x - g * per_group;
+        const int gh = (int)min((int64_t)kGroup, A.tile_rows - g * kGroup);
+        t = A.tile0 + (g * kGroup + rem % gh) * A.tiles_x + rem / gh;
+    }
+    const int tile_x0 = (int)(t % A.tiles_x) * T;
+    const int tile_y0 = (int)(A.row0 + (t / A.tiles_x) * (int64_t)T);
+    const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(tile);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int L = A.L;
+    // this thread's cell of levels >= 3 / LL: level lc (L + 1 = LL), subband bc, plane cell (ic, jc)
+    int lc = L + 1, bc = 0, ic, jc;
+    {
+        int c = tid;
+        for (int l = 3; l <= L; l++) {
+            const int q = T >> l, n = 3 * q * q;
+            if (c < n) { lc = l; bc = c / (q * q); c -= bc * q * q; break; }
+            c -= n;
+        }
+        const int q = T >> (lc <= L ? lc : L);
+        ic = c % q; jc = c / q;
+    }
+    const int lcs = lc <= L ? lc : L;            // LL moves with level L (R-A6, R-A8)
+    float2 h1[12], h2[3], hc;
+#pragma unroll
+    for (int k = 0; k < 12; k++) h1[k] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 3; k++) h2[k] = make_float2(0.f, 0.f);
+    hc = make_float2(0.f, 0.f);
+    const int cm = (1 << A.cls_bits) - 1;
+    const unsigned long long b0 = bptr[t], b1 = bptr[t + 1];
+    for (unsigned long long pb = b0; pb < b1; pb += kGatherBatch) {
+        const int np = (int)min((unsigned long long)kGatherBatch, b1 - pb);
+        __syncthreads();
+        if (tid < np) {
+            const int4 q = pconv[bidx[pb + tid]];
+            const int tb_ = table_of(q.x, q.y, q.z, A.cls_bits);
+            const int H = kd[tb_].H;
+            GatherPoint P;
+            P.tp = dense + dd[tb_].coef_off;
+            P.s = kd[tb_].side;
+            P.a = __int_as_float(q.w);
+            int off = 0;
+#pragma unroll
+            for (int l = 1; l <= kMaxLevels; l++) {
+                const int h = 1 << (l - 1), sl = P.s >> l;
+                const int sx = A.cls_bits ? (q.x & ~cm) : ((q.x + h) >> l) << l;
+                const int sy = A.cls_bits ? (q.y & ~cm) : ((q.y + h) >> l) << l;
+                // exact: every term is a multiple of 2^l
+                P.o[l - 1] = make_int2((tile_x0 - sx + H) >> l, (tile_y0 - sy + H) >> l);
+                P.off[l - 1] = off;
+                if (l <= L) off += 3 * sl * sl;
+            }
+            {
+                const int s1 = P.s >> 1;
+                P.in1 = P.o[0].x >= 0 && P.o[0].x + T / 2 <= s1 && P.o[0].y >= 0 && P.o[0].y + T / 2 <= s1;
+            }
+            P.off[kMaxLevels] = off;   // LL right after level L (set in the loop above when L < 6)
+            gp[tid] = P;
+        }
+        __syncthreads();
+        for (int j = 0; j < np; j++) {
+            const GatherPoint &G = gp[j];
+            const float a = G.a;
+            const int s = G.s;
+            const float2 *__restrict__ tp = G.tp;
+            {   // level 1: 12 rows of 32 cells per warp (32-bit offsets from the table pointer)
+                const int s1 = s >> 1, d8 = 8 * s1, P1 = s1 * s1;
+                const int2 o = G.o[0];
+                const int ox = o.x + lane, oy = o.y + w;
+                const float2 *__restrict__ p = tp + (oy * s1 + ox);
+                if (G.in1) {        // the whole 32 x 32 window inside the table: no checks
+#pragma unroll
+                    for (int k = 0; k < 12; k++) {
+                        const float2 v = __ldg(p + ((k >> 2) * P1 + (k & 3) * d8));
+                        h1[k].x = fmaf(a, v.x, h1[k].x);
+                        h1[k].y = fmaf(a, v.y, h1[k].y);
+                    }
+                } else {
+                    const bool cok = (unsigned)ox < (unsigned)s1;
+#pragma unroll
+                    for (int k = 0; k < 12; k++) {
+                        if (cok && (unsigned)(oy + 8 * (k & 3)) < (unsigned)s1) {
+                            const float2 v = __ldg(p + ((k >> 2) * P1 + (k & 3) * d8));
+                            h1[k].x = fmaf(a, v.x, h1[k].x);
+                            h1[k].y = fmaf(a, v.y, h1[k].y);
+                        }
+                    }
+                }
+            }
+            {   // level 2: one row of 16 cells per half-warp, three planes
+                const int s2 = s >> 2;
+                const int2 o = G.o[1];
+                const int ox = o.x + (lane & 15), oy = o.y + 2 * w + (lane >> 4);
+                if ((unsigned)ox < (unsigned)s2 && (unsigned)oy < (unsigned)s2) {
+                    const float2 *__restrict__ p = tp + (G.off[1] + oy * s2 + ox);
+                    const int P2 = s2 * s2;
+#pragma unroll
+                    for (int k = 0; k < 3; k++) {
+                        const float2 v = __ldg(p + k * P2);
+                        h2[k].x = fmaf(a, v.x, h2[k].x);
+                        h2[k].y = fmaf(a, v.y, h2[k].y);
+                    }
+                }
+            }
+            {   // levels >= 3 / LL: one cell
+                const int sc = s >> lcs;
+                const int2 o = G.o[lcs - 1];
+                const int ox = o.x + ic, oy = o.y + jc;
+                if ((unsigned)ox < (unsigned)sc && (unsigned)oy < (unsigned)sc) {
+                    const float2 v = __ldg(tp + (G.off[lc - 1] + bc * sc * sc + oy * sc + ox));
+                    hc.x = fmaf(a, v.x, hc.x);
+                    hc.y = fmaf(a, v.y, hc.y);
+                }
+            }
+        }
+    }
+    // psi of the tile into the (swizzled) shared tile in the interleaved layout, then the epilogue
+    constexpr int M = kWinMargin, S = T + M;
+    auto cell = [&](int r, int x) -> float2 & {
+        return tile[(swz(tile_sa + 8u * (uint32_t)(M + r * S + x)) - tile_sa) >> 3];
+    };
+#pragma unroll
+    for (int k = 0; k < 12; k++) {   // level 1, subband b: pixel (2i + (b != 1), 2j + (b >= 1))
+        const int b = k >> 2, jr = w + 8 * (k & 3);
+        cell(2 * jr + (b >= 1), 2 * lane + (b != 1)) = h1[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; k++) {    // level 2: (4i + 2 (b != 1), 4j + 2 (b >= 1))
+        const int jr = 2 * w + (lane >> 4), ir = lane & 15;
+        cell(4 * jr + 2 * (k >= 1), 4 * ir + 2 * (k != 1)) = h2[k];
+    }
+    {
+        const int hh = lc <= L ? 1 << (lc - 1) : 0;
+        cell((jc << lcs) + (bc >= 1 ? hh : 0), (ic << lcs) + (bc != 1 ? hh : 0)) = hc;
+    }
+    __syncthreads();
+    tile_epilogue<T, NT>(tile, tile_sa, L, fused, qa, bits, psi, A.row0, A.n_h, tile_x0, tile_y0);
+}
+
 }  // namespace
+
+cudaError_t launch_gather(const void *d_bins, const void *d_tables, int L, int cls_bits, int tiles_x, int tiles_y,
+                          int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4, double pitch,
+                          uint8_t *bits, cudaStream_t s, int tile_row0, int tile_row1) {
+    constexpr int T = 64, M = kWinMargin, S = T + M;
+    if (L < 2) return cudaErrorInvalidValue;
+    if (tile_row1 < 0) tile_row1 = tiles_y;
+    GatherArgs A;
+    A.L = L; A.cls_bits = cls_bits; A.tiles_x = tiles_x; A.row0 = row0; A.n_h = n_h;
+    A.tile0 = (int64_t)tile_row0 * tiles_x;
+    A.tile_rows = tile_row1 - tile_row0;
+    const int64_t n_tiles = (int64_t)tiles_x * (tile_row1 - tile_row0);
+    const QArgs qa = make_qargs(print4, pitch, n_h);
+    const int smem = (M + T * S + M + 8) * (int)sizeof(float2);
+    cudaError_t e = cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (n_tiles > 0) {
+        count_launches(1);
+        gather_kernel<<<(unsigned)n_tiles, 256, smem, s>>>(d_bins, d_tables, A, psi, fused, qa, bits);
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_superpose(const void *d_bins, const void *d_tables, int T, int S, int L, int cls_bits, int tiles_x,
                              int tiles_y, int64_t row0, int64_t n_h, float2 *psi, int fused, const double *print4,

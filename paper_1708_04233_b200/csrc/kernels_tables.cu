@@ -304,7 +304,35 @@ __global__ void __launch_bounds__(256) ventries_kernel(void *tables, int n_tab, 
     }
 }
 
+// K2e (gather mode, wasabi.h WASABI_FLAG_GATHER): every kept canonical entry (level l, X, Y) of table d
+// written at its Mallat position (internal.h mallat_index) of d's dense wavelet table (side_d^2
+// complex64, zeroed beforehand).
+__global__ void __launch_bounds__(256) dense_fill_kernel(void *tables, int n_tab, int L) {
+    const TableHeader &h = hdr(tables);
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= h.total_entries) return;
+    const DDesc *dd = at<DDesc>(tables, h.ddesc_off);
+    const int32_t *ptr = at<int32_t>(tables, h.ptr_off);
+    const uint4 en = at<uint4>(tables, h.ent_off)[e];
+    int lo = 0, hi = n_tab;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (ptr[dd[mid].group_base] <= e) lo = mid; else hi = mid;
+    }
+    const int X = (int)(en.x & 0x3fffu), Y = (int)((en.x >> 14) & 0x3fffu);
+    float2 *dense = atw<float2>(tables, h.dense_off);
+    dense[dd[lo].coef_off + mallat_index(X, Y, dd[lo].side, L)] = make_float2(__uint_as_float(en.y), __uint_as_float(en.z));
+}
+
 }  // namespace
+
+cudaError_t launch_dense_fill(const TableHeader &h, void *d_tables, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((h.total_entries + 255) / 256);
+    if (blocks == 0) return cudaSuccess;
+    count_launches(1);
+    dense_fill_kernel<<<blocks, 256, 0, s>>>(d_tables, h.n_depth, h.levels);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_ventries(const TableHeader &h, void *d_tables, int pass, int32_t *cursor, cudaStream_t s) {
     const unsigned blocks = (unsigned)((h.total_entries + 255) / 256);

@@ -84,8 +84,12 @@ wasabi_status validate(const wasabi_params *P) {
     if (P->n_depth > 1 && !(P->z_max_m > P->z_min_m)) return fail(WASABI_EINVAL, "n_depth > 1 needs z_max > z_min");
     if (!(P->retention > 0) || P->retention > 1) return fail(WASABI_EINVAL, "retention must be in (0, 1]");
     if (llround(P->retention * 1e6) < 1) return fail(WASABI_EINVAL, "retention below 1 ppm");
-    if (P->flags & ~(uint32_t)(WASABI_FLAG_EXACT_SHIFT | WASABI_FLAG_COIFLET))
+    if (P->flags & ~(uint32_t)(WASABI_FLAG_EXACT_SHIFT | WASABI_FLAG_COIFLET | WASABI_FLAG_GATHER | WASABI_FLAG_SCATTER))
         return fail(WASABI_EINVAL, "unknown flags 0x%x", P->flags);
+    if ((P->flags & WASABI_FLAG_GATHER) && (P->flags & WASABI_FLAG_SCATTER))
+        return fail(WASABI_EINVAL, "WASABI_FLAG_GATHER and WASABI_FLAG_SCATTER are exclusive");
+    if ((P->flags & WASABI_FLAG_GATHER) && (P->tile != 64 || P->levels < 2 || (P->flags & WASABI_FLAG_COIFLET)))
+        return fail(WASABI_EINVAL, "WASABI_FLAG_GATHER needs tile 64, levels >= 2 and Haar tables");
     if ((P->flags & WASABI_FLAG_EXACT_SHIFT) && P->levels > 4)
         return fail(WASABI_EINVAL, "WASABI_FLAG_EXACT_SHIFT needs levels <= 4 (4^L offset-class tables per depth)");
     if (P->flags & WASABI_FLAG_COIFLET) {
@@ -95,6 +99,27 @@ wasabi_status validate(const wasabi_params *P) {
         if (P->n_h > 16384) return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET needs n_h <= 16384 (line synthesis in shared memory)");
     }
     return WASABI_OK;
+}
+
+// Superposition path (wasabi.h WASABI_FLAG_GATHER): the dense gather at high retention.
+bool use_gather(const wasabi_params &P) {
+    if (P.flags & WASABI_FLAG_GATHER) return true;
+    if (P.flags & WASABI_FLAG_SCATTER) return false;
+    return llround(P.retention * 1e6) >= 600000 && P.tile == 64 && P.levels >= 2 && !(P.flags & WASABI_FLAG_COIFLET);
+}
+
+// Step 2b launcher: the scatter kernel (window LUT) or the dense gather (WASABI_FLAG_GATHER tables);
+// the table buffer was built for the same parameters, so use_gather() names its layout.
+cudaError_t launch_sup(const wasabi_params &P, const void *d_bins, const void *d_tables, int64_t row0, int tiles_y,
+                       float2 *psi, int fused, const double *print4, uint8_t *bits, cudaStream_t s, int tile_row0 = 0,
+                       int tile_row1 = -1) {
+    const int T = P.tile, tiles_x = (int)(P.n_h / T);
+    const int cb = (P.flags & WASABI_FLAG_EXACT_SHIFT) ? P.levels : 0;
+    if (use_gather(P))
+        return launch_gather(d_bins, d_tables, P.levels, cb, tiles_x, tiles_y, row0, P.n_h, psi, fused, print4,
+                             P.pitch_m, bits, s, tile_row0, tile_row1);
+    return launch_superpose(d_bins, d_tables, T, T + kWinMargin, P.levels, cb, tiles_x, tiles_y, row0, P.n_h, psi,
+                            fused, print4, P.pitch_m, bits, s, tile_row0, tile_row1);
 }
 
 wasabi_status validate_band(const wasabi_params *P, int64_t row0, int64_t row1) {
@@ -162,6 +187,7 @@ struct Geo {
     double k, tan_theta, dz;
     int T, S, L, nd, nz, cb;   // nd = tables, nz = depth levels, cb = offset-class bits (R-A20)
     int wav = 0;               // 1: coif1 tables (R-A21)
+    int gather = 0;            // 1: dense gather superposition (WASABI_FLAG_GATHER / high retention)
     std::vector<int64_t> pre;  // coif: per level, (nd + 1) prefix of analysis work items
     size_t sc_work = 0, sc_tmp = 0, sc_pre = 0;
     std::vector<KDesc> kd;
@@ -186,6 +212,7 @@ wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
     g.cb = (P->flags & WASABI_FLAG_EXACT_SHIFT) ? P->levels : 0;
     g.nd = P->n_depth << (2 * g.cb);
     g.wav = (P->flags & WASABI_FLAG_COIFLET) ? 1 : 0;
+    g.gather = use_gather(*P) ? 1 : 0;
     g.k = 2.0 * kPi / P->wavelength_m;
     const double sigma = P->wavelength_m / (2.0 * P->pitch_m);
     g.tan_theta = sigma / std::sqrt(1.0 - sigma * sigma);
@@ -252,8 +279,8 @@ wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
             D.n_r = std::min(n, D.nnz);
         }
         entries += D.n_r;
-        if (ptr > (int64_t)INT32_MAX / 2 || entries * win_variants(1, g.cb) > (int64_t)INT32_MAX / 2 ||
-            ctas > (int64_t)INT32_MAX / 2 || vptr > (int64_t)INT32_MAX / 2)
+        if (ptr > (int64_t)INT32_MAX / 2 || ctas > (int64_t)INT32_MAX / 2 ||
+            (!g.gather && (entries * win_variants(1, g.cb) > (int64_t)INT32_MAX / 2 || vptr > (int64_t)INT32_MAX / 2)))
             return fail(WASABI_EINVAL, "table too large for 32-bit indices");
     }
     g.ctabase[g.nd] = (int32_t)ctas;
@@ -273,12 +300,18 @@ wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
     h.ptr_off = off; off = align_up(off + 4 * (size_t)(ptr + 1), 256);
     h.ent_off = off; off = align_up(off + 16 * (size_t)entries, 256);
     // window LUT: a level-l entry is stored once per variant (<= win_variants(1) copies)
+    if (g.gather) vptr = 0;                // gather mode: no window LUT (the dense tables instead)
+    g.total_vptrs = vptr;
+    h.gather = g.gather;
     h.total_vptrs = vptr;
-    h.vent_cap = win_variants(1, g.cb) * entries;
+    h.vent_cap = g.gather ? 0 : win_variants(1, g.cb) * entries;
     h.vptr_off = off; off = align_up(off + 4 * (size_t)(vptr + 1), 256);
     // + 32 entries of padding: the superposition kernel reads whole 32-entry chunks past a range end
     h.vval_off = off; off = align_up(off + 8 * (size_t)(h.vent_cap + 32), 256);
     h.vpos_off = off; off = align_up(off + 2 * (size_t)(h.vent_cap + 32), 256);
+    // dense wavelet tables (gather mode): table t at dense_off + 8 coef_off_t, side_t^2 complex64
+    h.dense_off = off;
+    if (g.gather) off = align_up(off + 8 * (size_t)coef, 256);
     h.table_bytes = off;
     g.table_bytes = off;
     // build scratch
@@ -457,6 +490,11 @@ wasabi_status wasabi_build_psf_tables(const wasabi_params *params, void *d_table
     CK(launch_scan_i32(reinterpret_cast<int32_t *>(tb + g.th.ptr_off), g.total_ptrs + 1, sb + g.sc_scan, stream),
        "scan ptr");
     CK(launch_groups(g.th, d_tables, cval, ckey, sel, 1, stream), "groups scatter");
+    if (g.gather) {   // dense tables: zeros, then every kept coefficient at its table position
+        CK(cudaMemsetAsync(tb + g.th.dense_off, 0, 8 * (size_t)g.total_coef, stream), "memset dense");
+        CK(launch_dense_fill(g.th, d_tables, stream), "dense fill");
+        return WASABI_OK;
+    }
     // the superposition kernel's window LUT, re-grouped from the canonical lists
     CK(cudaMemsetAsync(tb + g.th.vptr_off, 0, 4 * (size_t)(g.total_vptrs + 1), stream), "memset vptr");
     int32_t *cursor = reinterpret_cast<int32_t *>(sb + g.sc_cursor);
@@ -561,10 +599,8 @@ wasabi_status wasabi_superpose(const wasabi_params *params, const void *d_tables
     if (!d_tables || !d_bins || (!d_psi && row1 > row0)) return fail(WASABI_EINVAL, "NULL buffer");
     if (!aligned(d_psi, 16)) return fail(WASABI_EINVAL, "d_psi must be 16-byte aligned");
     const int T = params->tile;
-    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, cls_bits(*params), (int)(params->n_h / T),
-                        (int)((row1 - row0) / T),
-                        row0, params->n_h, reinterpret_cast<float2 *>(d_psi), 0, nullptr, params->pitch_m, nullptr,
-                        stream),
+    CK(launch_sup(*params, d_bins, d_tables, row0, (int)((row1 - row0) / T), reinterpret_cast<float2 *>(d_psi), 0,
+                  nullptr, nullptr, stream),
        "superpose");
     return WASABI_OK;
 }
@@ -584,10 +620,8 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
     double p4[4];
     if (print) { p4[0] = print->x_r_m; p4[1] = print->y_r_m; p4[2] = print->z_r_m; p4[3] = 1.0 / params->wavelength_m; }
     const int T = params->tile;
-    CK(launch_superpose(d_bins, d_tables, T, T + kWinMargin, params->levels, cls_bits(*params), (int)(params->n_h / T),
-                        (int)((row1 - row0) / T),
-                        row0, params->n_h, reinterpret_cast<float2 *>(d_u), 1, print ? p4 : nullptr, params->pitch_m,
-                        d_bits, stream),
+    CK(launch_sup(*params, d_bins, d_tables, row0, (int)((row1 - row0) / T), reinterpret_cast<float2 *>(d_u), 1,
+                  print ? p4 : nullptr, d_bits, stream),
        "superpose_inverse");
     return WASABI_OK;
 }
@@ -828,10 +862,8 @@ wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_pri
         double p4[4] = {print->x_r_m, print->y_r_m, print->z_r_m, 1.0 / params->wavelength_m};
         for (int ty = 0; ty < tiles_y; ty += chunk) {
             const int ty1 = std::min(tiles_y, ty + chunk);
-            CK(launch_superpose(ws + w.bins, ws + w.tables, T, T + kWinMargin, params->levels, cls_bits(*params),
-                                (int)(params->n_h / T), tiles_y, row0, params->n_h,
-                                h_u ? reinterpret_cast<float2 *>(d_field) : nullptr, 1, p4, params->pitch_m, d_bits,
-                                stream, ty, ty1),
+            CK(launch_sup(*params, ws + w.bins, ws + w.tables, row0, tiles_y,
+                          h_u ? reinterpret_cast<float2 *>(d_field) : nullptr, 1, p4, d_bits, stream, ty, ty1),
                "superpose_inverse chunk");
             CK(join(cs, stream), "chunk done");
             const size_t r0 = (size_t)ty * T, nr = (size_t)(ty1 - ty) * T;

@@ -48,13 +48,17 @@ def _case(seed):
 
 # WASABI_RANDOM_SEEDS=<n> widens the sweep (the default run keeps 12 seeds per mode)
 @pytest.mark.parametrize("seed", range(int(os.environ.get("WASABI_RANDOM_SEEDS", "12"))))
-@pytest.mark.parametrize("mode", ["haar", "exact", "coif"])
+@pytest.mark.parametrize("mode", ["haar", "exact", "coif", "gather"])
 def test_random_problem_parity(W, orc, seed, mode):
     import torch
     P, tile, pts, rng = _case(seed)
     kw = dict(exact=(mode == "exact"), wavelet=1 if mode == "coif" else 0)
+    gkw = {}
+    if mode == "gather":   # the dense gather superposition (WASABI_FLAG_GATHER: tile 64, L >= 2, Haar)
+        tile, P["levels"] = 64, max(2, P["levels"])
+        gkw = dict(path="gather")
     p = W.Params(P["wavelength"], P["pitch"], P["n_h"], P["n_depth"], P["levels"], P["z_min"], P["z_max"],
-                 P["retention"], tile, **kw)
+                 P["retention"], tile, **kw, **gkw)
     Po = orc.Params(**P, **kw)
     nb = P["n_h"] // tile
     t0 = int(rng.integers(0, nb))

@@ -135,3 +135,27 @@ def test_coif_mode_validation(W, kw, msg):
     p = W.Params.from_config(CONFIGS["C3"].replace(levels=3), wavelet=1, **kw)
     with pytest.raises(W.WasabiError, match=msg):
         W.psf_tables_bytes(p)
+
+
+@pytest.mark.parametrize("kw,msg", [(dict(path="gather", tile=128), "tile 64"),
+                                    (dict(path="gather", levels=1), "levels >= 2"),
+                                    (dict(path="gather", wavelet=1, levels=3), "Haar")])
+def test_gather_mode_validation(W, kw, msg):
+    p = W.Params.from_config(CONFIGS["C1"].replace(retention=1.0), **kw)
+    with pytest.raises(W.WasabiError, match=msg):
+        W.psf_tables_bytes(p)
+
+
+def test_gather_tables_replace_window_lut(W):
+    """WASABI_FLAG_GATHER: the table buffer holds the dense wavelet tables (sum of side^2 complex64)
+    instead of the window LUT; auto selects the gather at r >= 0.6 only."""
+    cfg = CONFIGS["C5"].replace(retention=1.0, levels=5)
+    tg, _ = W.psf_tables_bytes(W.Params.from_config(cfg, path="gather"))
+    ts, _ = W.psf_tables_bytes(W.Params.from_config(cfg, path="scatter"))
+    ta, _ = W.psf_tables_bytes(W.Params.from_config(cfg))
+    side2 = sum((2 * W.depth_geometry(W.Params.from_config(cfg), d)["H"]) ** 2 for d in range(cfg.n_depth))
+    assert ta == tg and tg != ts
+    assert tg >= 8 * side2
+    t5, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.5)))
+    t5s, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.5), path="scatter"))
+    assert t5 == t5s

@@ -21,6 +21,9 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tile", type=int, default=None)
 ap.add_argument("--fused", action="store_true", help="time superpose_inverse (fused path, as bench.py)")
 ap.add_argument("--pkg", default=None)
+ap.add_argument("--retention", type=float, default=None)
+ap.add_argument("--n", type=int, default=None, help="point count (default: the config's)")
+ap.add_argument("--path", default="auto", choices=["auto", "gather", "scatter"])
 ap.add_argument("--no-u", action="store_true", help="fused: bits only (no u write)")
 ap.add_argument("--no-bits", action="store_true", help="fused: u only (no binarisation)")
 ap.add_argument("--dump", default=None, help="np.save psi (after the timed superposes) to this path")
@@ -28,8 +31,10 @@ a = ap.parse_args()
 cfg = CONFIGS[a.config]
 if a.tile:
     cfg = cfg.replace(tile=a.tile)
-p = W.Params.from_config(cfg)
-pts = make_points(cfg)
+if a.retention:
+    cfg = cfg.replace(retention=a.retention)
+p = W.Params.from_config(cfg, path=a.path)
+pts = make_points(cfg, n=a.n)
 pl = W.Pipeline(p, len(pts), a.row0, a.row0 + a.rows, want_u=not a.no_u, want_bits=not a.no_bits)
 d = torch.from_numpy(pts).cuda()
 pl.run(d)

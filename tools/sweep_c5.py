@@ -55,6 +55,8 @@ def main():
     ap.add_argument("--wavelet", type=int, default=0, help="1: coif1 tables (WASABI_FLAG_COIFLET, R-A21)")
     ap.add_argument("--depths", type=int, default=None)
     ap.add_argument("--no-d1", action="store_true")
+    ap.add_argument("--path", default="auto", choices=["auto", "gather", "scatter"],
+                    help="superposition kernel (WASABI_FLAG_GATHER / _SCATTER; auto: gather iff r >= 0.6)")
     ap.add_argument("--out", default="gpurun_out/c5_sweep.jsonl")
     a = ap.parse_args()
     base = CONFIGS["C5"]
@@ -96,7 +98,7 @@ def main():
         del dense, bins_ref, tabs
         for r in [float(x) for x in a.rs.split(",")]:
             cfg = base.replace(retention=r)
-            p = W.Params.from_config(cfg, exact=a.exact, wavelet=a.wavelet)
+            p = W.Params.from_config(cfg, exact=a.exact, wavelet=a.wavelet, path=a.path)
             pl = W.Pipeline(p, n, 0, p.n_h)
             reps = 3 if n < 10_000_000 else 1
             t_w = timed(lambda: pl.run(d_pts), reps=reps)
@@ -104,6 +106,7 @@ def main():
             acc = W.count_accumulations(p, pl.tables, d_pts, 0, p.n_h, s8)
             st = W.bins_stats(pl.bins)
             rec = {"n_points": n, "retention": r, "aligned": a.aligned, "exact": a.exact, "wavelet": a.wavelet,
+                   "path": a.path if a.path != "auto" else ("gather" if r >= 0.6 and a.wavelet == 0 else "scatter"),
                    "levels": cfg.levels, "n_depth": cfg.n_depth, "wasabi_ms": t_w,
                    "gpix_per_s": p.n_h ** 2 / (t_w * 1e-3) / 1e9, "points_per_s": n / (t_w * 1e-3),
                    "fused_kernel_ms": t_k, "accumulations": acc,
