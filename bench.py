@@ -52,9 +52,10 @@ def _peaks():
     return hbm, fp
 
 
-def _workload(cfg):
+def _workload(cfg, wavelet=0):
     return (f"{cfg.name}: {cfg.n_h}x{cfg.n_h} hologram, {cfg.n_points:,} points ({cfg.kind}), "
-            f"{cfg.n_depth} levels in [{cfg.z_min * 1e3:g},{cfg.z_max * 1e3:g}] mm, L={cfg.levels} Haar, "
+            f"{cfg.n_depth} levels in [{cfg.z_min * 1e3:g},{cfg.z_max * 1e3:g}] mm, L={cfg.levels} "
+            f"{'coif1' if wavelet else 'Haar'}, "
             f"r={cfg.retention:g}, lambda={cfg.wavelength * 1e9:g} nm, pitch={cfg.pitch * 1e6:g} um")
 
 
@@ -259,7 +260,9 @@ def run_ours(args, cfg):
         dist.all_gather(parts, t)
         return [p.tolist() for p in parts]
 
-    p = W.Params.from_config(cfg)
+    p = W.Params.from_config(cfg, wavelet=args.wavelet)
+    if args.wavelet:
+        args.unfused = True     # coiflets (R-A21): the synthesis is not tile-local -> superpose + inverse_wt
     pts = make_points(cfg)
     n = len(pts)
     d_pts = torch.from_numpy(pts).to(dev)
@@ -457,7 +460,9 @@ def run_ours(args, cfg):
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded generators, inputs/; the paper's 3D model is unavailable)",
-               "config": {"workload": _workload(cfg), "path": "unfused" if args.unfused else "fused",
+               "config": {"workload": _workload(cfg, args.wavelet),
+                          "path": ("unfused (coif1 halo band + line synthesis)" if args.wavelet else "unfused")
+                          if args.unfused else "fused",
                           "n_h": cfg.n_h, "n_points": n, "levels": cfg.levels, "retention": cfg.retention,
                           "n_depth": cfg.n_depth, "tile": p.tile, "rows_per_gpu": rows,
                           "parallelism": f"row bands x{world} ({mode})", "l2": l2},
@@ -560,6 +565,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--unfused", action="store_true", help="time the 4-call path (psi through HBM)")
+    ap.add_argument("--levels", type=int, default=None, help="override the config's wavelet levels L")
+    ap.add_argument("--wavelet", type=int, default=0, choices=[0, 1],
+                    help="1: coif1 tables (WASABI_FLAG_COIFLET, R-A21; implies --unfused)")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default) or gloo (test mode)")
     ap.add_argument("--same-device", action="store_true", help="test mode: all ranks on cuda:0")
     ap.add_argument("--direct", action="store_true",
@@ -572,6 +580,10 @@ def main():
         cfg = cfg.replace(retention=args.retention)
     if args.tile:
         cfg = cfg.replace(tile=args.tile)
+    if args.levels:
+        cfg = cfg.replace(levels=args.levels)
+    elif args.wavelet:
+        cfg = cfg.replace(levels=min(cfg.levels, 3))    # "coiflets as the wavelets at level 3"
     if args.impl == "reference":
         run_reference(args, cfg)
     elif args.direct:

@@ -82,7 +82,7 @@ typedef struct {
 #define WASABI_FLAG_EXACT_SHIFT 1u
 
 /* Coiflets, the paper's wavelet ("coiflets as the wavelets at level 3"; SURVEY.md
- * §8(f) NEXT-2, reading R-A21; needs levels <= 4, n_h <= 16384, not with EXACT_SHIFT).  The tables
+ * §8(f) NEXT-2, reading R-A21; needs levels <= 4, not with EXACT_SHIFT).  The tables
  * use the coif1 filter bank (6 taps) on the interleaved layout with zero extension, padded so every
  * nonzero coefficient is kept in the table; the superposition is unchanged.  The inverse is not
  * block-local: u on rows [row0, row1) needs psi on the HALO band [max(0, row0 - H), min(n_h, row1 +

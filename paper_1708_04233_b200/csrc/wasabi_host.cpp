@@ -96,7 +96,6 @@ wasabi_status validate(const wasabi_params *P) {
         if (P->flags & WASABI_FLAG_EXACT_SHIFT)
             return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET cannot be combined with WASABI_FLAG_EXACT_SHIFT");
         if (P->levels > 4) return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET needs levels <= 4 (psi halo of one tile)");
-        if (P->n_h > 16384) return fail(WASABI_EINVAL, "WASABI_FLAG_COIFLET needs n_h <= 16384 (line synthesis in shared memory)");
     }
     return WASABI_OK;
 }

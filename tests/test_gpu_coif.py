@@ -7,7 +7,7 @@ chain's closed form: r = 100%, aligned points -> u equals the GPU direct sum."""
 import numpy as np
 import pytest
 
-from helpers import field_check, CONFIGS, gpu_params, make_points, orc_params, rel_l2
+from helpers import field_check, field_np, CONFIGS, gpu_params, make_points, orc_params, rel_l2
 from test_gpu_parity import W, _check_fields, _direct_gpu, _gpu_run, _tables  # noqa: F401
 
 pytestmark = pytest.mark.gpu
@@ -101,3 +101,39 @@ def test_coif_fused_entry_refuses(W):
     pl = W.Pipeline(p, 10, 0, p.n_h)
     with pytest.raises(W.WasabiError, match="COIFLET"):
         W.superpose_inverse(p, pl.tables, pl.bins, 0, p.n_h, W.PrintParams(), pl.field, pl.bits)
+
+
+@pytest.mark.parametrize("row0,x0", [(32768, 32768), (0, 65536 - 1024)])
+def test_coif_c4_band_paper_scale(W, orc, row0, x0):
+    """Coiflets at the paper's scale (PAPER.md:106 "coiflets as the wavelets at level 3", :128 a
+    65,536^2 hologram): C4 with L = 3 on a 1024-row band (psi on its halo band, then the coif1 line
+    synthesis), u and psi element-wise and in rel L2 within 1e-5 of the oracle on a 1024^2 window of it,
+    bits identical outside the fixed threshold band (a central window, and a hologram corner where
+    the zero boundary of R-A21 applies)."""
+    import torch
+    from helpers import REF, bits_check, oracle_window, parity_log
+    cfg = CONFIGS["C4"].replace(levels=3)
+    pts = make_points(cfg)
+    p = gpu_params(cfg, wavelet=1)
+    row1, w = row0 + 1024, 1024
+    pl = W.Pipeline(p, len(pts), row0, row1)
+    d = torch.from_numpy(pts).cuda()
+    pl.build_tables()
+    pl.bin(d)
+    pl.superpose()
+    torch.cuda.synchronize()
+    psi_g = field_np(pl.psi_band[row0 - pl.e0:row1 - pl.e0, x0:x0 + w])
+    pl.inverse()
+    torch.cuda.synchronize()
+    u_g = field_np(pl.field[:, x0:x0 + w])
+    bits_g = pl.bits[:, x0 // 8:(x0 + w) // 8].cpu().numpy()
+    P = orc_params(orc, cfg, wavelet=1)
+    u_o, psi_o, bits_o, I_o = oracle_window(P, pts, x0, row0, w, 1024)
+    e_psi, m_psi = field_check(psi_g, psi_o)
+    e_u, m_u = field_check(u_g, u_o)
+    bc = bits_check(bits_g, bits_o, I_o, u_g, u_o)
+    parity_log(dict(case=f"C4 coif1 L=3 [{x0},{x0 + w}) x [{row0},{row1})", rel_psi=e_psi, max_psi=m_psi,
+                    rel_u=e_u, max_u=m_u, **bc))
+    assert np.linalg.norm(u_o) > 0
+    assert max(e_psi, m_psi, e_u, m_u) <= 1e-5, (e_psi, m_psi, e_u, m_u)
+    assert bc["bad"] == 0, bc

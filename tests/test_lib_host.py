@@ -129,8 +129,7 @@ def test_coif_host_geometry_equals_oracle(W, orc, name, kw):
     assert p.halo_rows() == max(64, p.tile)
 
 
-@pytest.mark.parametrize("kw,msg", [(dict(levels=5), "levels <= 4"), (dict(exact=True), "EXACT_SHIFT"),
-                                    (dict(n_h=32768), "n_h <= 16384")])
+@pytest.mark.parametrize("kw,msg", [(dict(levels=5), "levels <= 4"), (dict(exact=True), "EXACT_SHIFT")])
 def test_coif_mode_validation(W, kw, msg):
     p = W.Params.from_config(CONFIGS["C3"].replace(levels=3), wavelet=1, **kw)
     with pytest.raises(W.WasabiError, match=msg):
@@ -159,3 +158,11 @@ def test_gather_tables_replace_window_lut(W):
     t5, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.5)))
     t5s, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.5), path="scatter"))
     assert t5 == t5s
+
+
+def test_coif_paper_scale_accepted(W):
+    """The coiflet mode at the paper's scale (PAPER.md:106 level 3, :128 65,536^2): the line synthesis
+    streams rolling windows along rows and columns, so N_h is not capped."""
+    p = W.Params.from_config(CONFIGS["C4"].replace(levels=3), wavelet=1)
+    tb, sb = W.psf_tables_bytes(p)
+    assert tb > 0 and sb > 0 and p.halo_rows() == 64
