@@ -308,14 +308,16 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     const unsigned long long b1 = bptr[t + 1];
     unsigned long long pb = bptr[t];
 
-    // batch state: lane = point; per level slot j its range (beg, len) and smem base
-    float a_l = 0.f;
+    // batch state: lane = point; per level slot j its range: first entry beg and pk = (smem base << 16)
+    // | length; the CURRENT batch (beg, pk, a_l) and the NEXT one (nbeg, npk, na), loaded while the
+    // current batch's chunks stream (software-pipelined batches, WASABI_PIPE)
+    float a_l = 0.f, na = 0.f;
     constexpr int kSlots = WASABI_CLS == 2 ? 3 : 4;   // level slots per warp
-    int beg[4], len[4], base[4];
+    int beg[4] = {0, 0, 0, 0}, pk[4] = {0, 0, 0, 0}, nbeg[4] = {0, 0, 0, 0}, npk[4] = {0, 0, 0, 0};
     const int cb = EX ? A.L : 0;               // offset-class bits (R-A20) or 0
     const int cmask = (1 << cb) - 1;
-    auto range = [&](int l, int ix, int iy, int H, int side, int vrow, bool ok, int &b, int &n, int &bs) {
-        b = 0; n = 0; bs = 0;
+    auto range = [&](int l, int ix, int iy, int H, int side, int vrow, bool ok, int &b, int &p) {
+        b = 0; p = 0;
         if (l == 0) return;
         const int h = 1 << (l - 1);
         // R-A8 level shift, or the 2^L-aligned shift of the offset-class tables (R-A20)
@@ -329,19 +331,21 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         const int k = (o - (v << lq) + kWinRows) >> 5;
         const int ncol = win_cols(side, l);
         const int xa = max(xs >> lg, 0), xb = min((xs + T + (1 << lg) - 1) >> lg, ncol);
+        int n = 0;
         if (ok && xa < xb) {
             const int row = vrow + (v * win_bands(side) + k) * (ncol + 1);
             b = __ldg(vptr + row + xa);
             n = __ldg(vptr + row + xb) - b;
         }
-        bs = strip_base - xs;
+        p = (int)(((uint32_t)(strip_base - xs) << 16) | (uint32_t)n);   // |base| < 2^15, length < 2^16
     };
     // the point records of the next batch are loaded one batch ahead and its bin indices two
     // batches ahead (the loads overlap the ring): two dependent round trips off the batch phase
     // (batches are 32 points but the last)
     uint32_t nidx = pb + 32 + lane < b1 ? __ldg(bidx + pb + 32 + lane) : 0u;
     int4 qn = pb + lane < b1 ? __ldg(pconv + __ldg(bidx + pb + lane)) : make_int4(0, 0, 0, 0);
-    auto load_batch = [&]() -> bool {
+    // the next batch with any work from pb on into (ob, op, oa); false: none left
+    auto fetch = [&](int *ob, int *op, float &oa) -> bool {
         while (pb < b1) {
             const int nq = (int)min((unsigned long long)32, b1 - pb);
             const bool ok = lane < nq;
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             int2 hv = make_int2(0, 0);          // (H, first window-LUT pointer slot)
             if (ok) hv = __ldg(reinterpret_cast<const int2 *>(&kd[table_of(q.x, q.y, q.z, cb)].H));
             pb += nq;
-            a_l = __int_as_float(q.w);
+            oa = __int_as_float(q.w);
             const int side = 2 * hv.x + (EX ? 1 << A.L : 0);
             // pointer rows of the class's levels: level l starts after the slots of levels < l
             int vr[4];
@@ -364,21 +368,13 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
                     vr[j] = acc;
                 }
             }
-            range(lv0, q.x, q.y, hv.x, side, vr[0], ok, beg[0], len[0], base[0]);
-            range(lv1, q.x, q.y, hv.x, side, vr[1], ok, beg[1], len[1], base[1]);
-            range(lv2, q.x, q.y, hv.x, side, vr[2], ok, beg[2], len[2], base[2]);
-            if (kSlots > 3) range(lv3, q.x, q.y, hv.x, side, vr[3], ok, beg[3], len[3], base[3]);
+            range(lv0, q.x, q.y, hv.x, side, vr[0], ok, ob[0], op[0]);
+            range(lv1, q.x, q.y, hv.x, side, vr[1], ok, ob[1], op[1]);
+            range(lv2, q.x, q.y, hv.x, side, vr[2], ok, ob[2], op[2]);
+            if (kSlots > 3) range(lv3, q.x, q.y, hv.x, side, vr[3], ok, ob[3], op[3]);
             bool any = false;
 #pragma unroll
-            for (int j = 0; j < kSlots; j++) {
-                any |= __any_sync(kFull, len[j] > 0);
-                if (WASABI_PF && len[j] > 0) {
-                    const int e0 = beg[j] & ~1, e1 = (beg[j] + len[j] + 1) & ~1;   // 16-byte granules
-                    prefetch_l2(vval + e0, 8u * (uint32_t)(e1 - e0));
-                    const int p0 = beg[j] & ~7, p1 = (beg[j] + len[j] + 7) & ~7;
-                    prefetch_l2(vpos + p0, 2u * (uint32_t)(p1 - p0));
-                }
-            }
+            for (int j = 0; j < kSlots; j++) any |= __any_sync(kFull, (op[j] & 0xffff) != 0);
             if (any) return true;
         }
         return false;
@@ -389,34 +385,41 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     uint32_t c_sa = tile_sa;
     unsigned gm = 0u;
     float c_a = 0.f;
-    bool have = false;
+    bool have = false, nhave = false, refill = false;
     int s_beg = 0, s_pk = 0;                 // this lane's range for slot gj: first entry, (base << 16) | length
     auto select_slot = [&]() {
         s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : (kSlots == 3 || gj == 2) ? beg[2] : beg[3];
-        const int sl = gj == 0 ? len[0] : gj == 1 ? len[1] : (kSlots == 3 || gj == 2) ? len[2] : len[3];
-        const int sb = gj == 0 ? base[0] : gj == 1 ? base[1] : (kSlots == 3 || gj == 2) ? base[2] : base[3];
-        s_pk = (int)(((uint32_t)sb << 16) | (uint32_t)sl);   // |base| < 2^15, length < 2^16
-        gm = __ballot_sync(kFull, sl > 0);
+        s_pk = gj == 0 ? pk[0] : gj == 1 ? pk[1] : (kSlots == 3 || gj == 2) ? pk[2] : pk[3];
+        gm = __ballot_sync(kFull, (s_pk & 0xffff) != 0);
     };
     auto next_range = [&]() {
         while (gm == 0u) {
-            if (++gj >= kSlots) {    // batch exhausted: the outer loop loads the next one
-                have = false;
-                c_beg = c_end = 0;    // an empty range: the remaining ring slots idle
-                return;
+            if (++gj >= kSlots) {    // batch exhausted: continue with the prefetched next batch, if any
+                if (!nhave) {
+                    have = false;
+                    c_beg = c_end = 0;    // an empty range: the remaining ring slots idle
+                    return;
+                }
+#pragma unroll
+                for (int j = 0; j < kSlots; j++) { beg[j] = nbeg[j]; pk[j] = npk[j]; }
+                a_l = na;
+                nhave = false;
+                refill = true;        // the ring loop fetches the batch after it
+                gj = 0;
             }
             select_slot();
         }
         const int p = __ffs(gm) - 1;
         gm &= gm - 1u;
         c_beg = __shfl_sync(kFull, s_beg, p);
-        const int pk = __shfl_sync(kFull, s_pk, p);   // 3 shuffles per range: they use the L1TEX data pipe
-        c_end = c_beg + (pk & 0xffff);
-        c_sa = tile_sa + 8u * (uint32_t)(pk >> 16);
+        const int q = __shfl_sync(kFull, s_pk, p);   // 3 shuffles per range: they use the L1TEX data pipe
+        c_end = c_beg + (q & 0xffff);
+        c_sa = tile_sa + 8u * (uint32_t)(q >> 16);
         c_a = __shfl_sync(kFull, a_l, p);
         have = true;
     };
-    if (load_batch()) {
+    if (fetch(beg, pk, a_l)) {
+        nhave = fetch(nbeg, npk, na);
         gj = 0;
         select_slot();
         next_range();
@@ -460,27 +463,27 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         o.y = fmaf(ra[u], rv[u].y, o.y);                                            \
         sts2(sa, o);                                                                \
     } while (0)
-    // one batch at a time: the ring drains at the end of a batch and the next batch is loaded here,
-    // so the batch code is inlined once (the kernel fits the instruction cache: 8.2k -> 2.9k SASS
-    // instructions, -10% at full C4 against loading batches inside the ring)
-    bool batch = have;
-    while (batch) {
+    // Batches are software-pipelined: when the range generator exhausts a batch it continues with the
+    // prefetched next one (a register swap) and flags a refill; the ring loop then leaves its unrolled
+    // body with the chunks of the new batch in flight, fetches the batch after it (the window-pointer
+    // loads overlap those chunks) and re-enters without draining.  The batch code stays inlined once
+    // (fetch, outside the ring body).  The ring drains only at the tile's last batch.
+    if (have) {
 #pragma unroll
         for (int u = 0; u < kD; u++) WASABI_PREFETCH(u);
-        bool more = true;
-        while (more) {
-            more = have;
+        while (true) {
+            bool more = true;
+            while (more) {
+                more = have && !refill;
 #pragma unroll
-            for (int u = 0; u < kD; u++) {
-                WASABI_CONSUME(u);
-                WASABI_PREFETCH(u);
+                for (int u = 0; u < kD; u++) {
+                    WASABI_CONSUME(u);
+                    WASABI_PREFETCH(u);
+                }
             }
-        }
-        batch = load_batch();
-        if (batch) {
-            gj = 0;
-            select_slot();
-            next_range();
+            if (!refill) break;                  // drained: no batch left
+            refill = false;
+            nhave = fetch(nbeg, npk, na);
         }
     }
 #undef WASABI_PREFETCH
