@@ -93,12 +93,15 @@ typedef struct {
 
 /* Dense gather superposition (the r -> 100% regime).  Eq.(2) is a sum of
  * sparse kept coefficients; at high retention the kept set is nearly dense and a per-pixel GATHER from
- * a dense wavelet-domain table (kept value or 0; one (side x side) complex64 table per PSF table) beats
- * the scatter of the kept list.  Each pixel of level l (R-A6) reads table(X - s_l(ix) + H, Y - s_l(iy)
- * + H) for every point of its tile's bin, in bin order: unkept coefficients add an exact 0, so psi is
- * BIT-IDENTICAL to the scatter path.  Default (neither flag): gather iff retention >= 0.6, tile == 64,
- * levels >= 2 and not coiflets; the flags force one path (GATHER needs tile 64, levels >= 2, Haar).
- * In gather mode the table buffer holds the dense tables instead of the superposition's window LUT. */
+ * a dense wavelet-domain table (kept value or 0; one side^2 complex64 table per PSF table, in Mallat
+ * subband-planar order) beats the scatter of the kept list.  Each pixel of level l (R-A6) reads its
+ * table at (pixel - s_l + H) for every point of its tile's bin, in depth-major order (reading R-A22:
+ * chunks of up to 1024 bin points, each sorted by (depth level, bin position), so the CTAs resident
+ * at one time read a few depths' tables at a time): psi equals the scatter path's up to the fp32
+ * rounding of the reordered sum, and is itself bitwise independent of the band split.  Default
+ * (neither flag): gather iff retention >= 0.25 (measured crossover at C5), tile == 64, levels >= 2 and not coiflets; the flags
+ * force one path (GATHER needs tile 64, levels >= 2, Haar).  In gather mode the table buffer holds
+ * the dense tables instead of the superposition's window LUT. */
 #define WASABI_FLAG_GATHER 4u
 #define WASABI_FLAG_SCATTER 8u
 

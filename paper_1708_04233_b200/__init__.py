@@ -59,7 +59,7 @@ class Params:
     tile: int = 64
     exact: bool = False   # WASABI_FLAG_EXACT_SHIFT: offset-class tables (R-A20)
     wavelet: int = 0      # 0 Haar; 1 WASABI_FLAG_COIFLET: coif1, the paper's coiflets (R-A21, NEXT-2)
-    path: str = "auto"    # superposition: "auto" (gather iff r >= 0.6), "gather" or "scatter" (wasabi.h)
+    path: str = "auto"    # superposition: "auto" (gather iff r >= 0.25), "gather" or "scatter" (wasabi.h)
 
     @staticmethod
     def from_config(cfg, **kw) -> "Params":

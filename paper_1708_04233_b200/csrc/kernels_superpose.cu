@@ -533,6 +533,7 @@ struct GatherPoint {          // one point of a batch, per tile
     int pad;
 };
 constexpr int kGatherBatch = 64;
+constexpr int kGatherChunk = 1024;   // bin points sorted by depth at a time (keys: depth << 10 | index)
 
 __global__ void __launch_bounds__(256, 3) gather_kernel(const void *__restrict__ d_bins,
                                                         const void *__restrict__ d_tables, GatherArgs A,
@@ -585,11 +586,34 @@ __global__ void __launch_bounds__(256, 3) gather_kernel(const void *__restrict__
     hc = make_float2(0.f, 0.f);
     const int cm = (1 << A.cls_bits) - 1;
     const unsigned long long b0 = bptr[t], b1 = bptr[t + 1];
-    for (unsigned long long pb = b0; pb < b1; pb += kGatherBatch) {
-        const int np = (int)min((unsigned long long)kGatherBatch, b1 - pb);
+    // depth-major order (reading R-A22): the bin is taken in chunks of up to kGatherChunk points (in
+    // bin order), each chunk sorted by (depth level, position in the bin); the CTAs resident at one
+    // time then read the dense tables of a few depths at a time (L2 reuse) instead of all of them
+    __shared__ uint32_t skey[kGatherChunk];
+    for (unsigned long long cbeg = b0; cbeg < b1; cbeg += kGatherChunk) {
+    const int nc = (int)min((unsigned long long)kGatherChunk, b1 - cbeg);
+    int sz = 64;
+    while (sz < nc) sz <<= 1;
+    __syncthreads();
+    for (int i = tid; i < sz; i += NT)
+        skey[i] = i < nc ? ((uint32_t)pconv[bidx[cbeg + i]].z << 10) | (uint32_t)i : 0xffffffffu;
+    for (int k = 2; k <= sz; k <<= 1) {          // bitonic sort, ascending (keys are distinct)
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            __syncthreads();
+            for (int i = tid; i < sz; i += NT) {
+                const int ij = i ^ jj;
+                if (ij > i) {
+                    const uint32_t x = skey[i], y = skey[ij];
+                    if ((x > y) == ((i & k) == 0)) { skey[i] = y; skey[ij] = x; }
+                }
+            }
+        }
+    }
+    for (int pb = 0; pb < nc; pb += kGatherBatch) {
+        const int np = min(kGatherBatch, nc - pb);
         __syncthreads();
         if (tid < np) {
-            const int4 q = pconv[bidx[pb + tid]];
+            const int4 q = pconv[bidx[cbeg + (skey[pb + tid] & 1023u)]];
             const int tb_ = table_of(q.x, q.y, q.z, A.cls_bits);
             const int H = kd[tb_].H;
             GatherPoint P;
@@ -670,6 +694,7 @@ __global__ void __launch_bounds__(256, 3) gather_kernel(const void *__restrict__
                 }
             }
         }
+    }
     }
     // psi of the tile into the (swizzled) shared tile in the interleaved layout, then the epilogue
     constexpr int M = kWinMargin, S = T + M;

@@ -104,7 +104,7 @@ wasabi_status validate(const wasabi_params *P) {
 bool use_gather(const wasabi_params &P) {
     if (P.flags & WASABI_FLAG_GATHER) return true;
     if (P.flags & WASABI_FLAG_SCATTER) return false;
-    return llround(P.retention * 1e6) >= 600000 && P.tile == 64 && P.levels >= 2 && !(P.flags & WASABI_FLAG_COIFLET);
+    return llround(P.retention * 1e6) >= 250000 && P.tile == 64 && P.levels >= 2 && !(P.flags & WASABI_FLAG_COIFLET);
 }
 
 // Step 2b launcher: the scatter kernel (window LUT) or the dense gather (WASABI_FLAG_GATHER tables);

@@ -147,7 +147,7 @@ def test_gather_mode_validation(W, kw, msg):
 
 def test_gather_tables_replace_window_lut(W):
     """WASABI_FLAG_GATHER: the table buffer holds the dense wavelet tables (sum of side^2 complex64)
-    instead of the window LUT; auto selects the gather at r >= 0.6 only."""
+    instead of the window LUT; auto selects the gather at r >= 0.25 only."""
     cfg = CONFIGS["C5"].replace(retention=1.0, levels=5)
     tg, _ = W.psf_tables_bytes(W.Params.from_config(cfg, path="gather"))
     ts, _ = W.psf_tables_bytes(W.Params.from_config(cfg, path="scatter"))
@@ -155,8 +155,8 @@ def test_gather_tables_replace_window_lut(W):
     side2 = sum((2 * W.depth_geometry(W.Params.from_config(cfg), d)["H"]) ** 2 for d in range(cfg.n_depth))
     assert ta == tg and tg != ts
     assert tg >= 8 * side2
-    t5, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.5)))
-    t5s, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.5), path="scatter"))
+    t5, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.2)))
+    t5s, _ = W.psf_tables_bytes(W.Params.from_config(cfg.replace(retention=0.2), path="scatter"))
     assert t5 == t5s
 
 

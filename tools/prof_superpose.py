@@ -24,6 +24,7 @@ ap.add_argument("--pkg", default=None)
 ap.add_argument("--retention", type=float, default=None)
 ap.add_argument("--n", type=int, default=None, help="point count (default: the config's)")
 ap.add_argument("--path", default="auto", choices=["auto", "gather", "scatter"])
+ap.add_argument("--sort-depth", action="store_true", help="experiment: permute the points by depth (stable)")
 ap.add_argument("--no-u", action="store_true", help="fused: bits only (no u write)")
 ap.add_argument("--no-bits", action="store_true", help="fused: u only (no binarisation)")
 ap.add_argument("--dump", default=None, help="np.save psi (after the timed superposes) to this path")
@@ -35,11 +36,20 @@ if a.retention:
     cfg = cfg.replace(retention=a.retention)
 p = W.Params.from_config(cfg, path=a.path)
 pts = make_points(cfg, n=a.n)
+if a.sort_depth:
+    import numpy as np
+    pts = pts[np.argsort(pts[:, 2], kind="stable")]
 pl = W.Pipeline(p, len(pts), a.row0, a.row0 + a.rows, want_u=not a.no_u, want_bits=not a.no_bits)
 d = torch.from_numpy(pts).cuda()
 pl.run(d)
 torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import Clocks  # noqa: E402
+clocks = Clocks(0, "/tmp/prof_superpose_clocks.csv")
+clocks.start()
+import time  # noqa: E402
+time.sleep(0.3)
 ev[0].record()
 for _ in range(a.reps):
     if a.fused:
@@ -48,8 +58,9 @@ for _ in range(a.reps):
         pl.superpose()
 ev[1].record()
 torch.cuda.synchronize()
+ck = clocks.stop()
 st = W.bins_stats(pl.bins)
-print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} {('fused' + (' no-u' if a.no_u else '') + (' no-bits' if a.no_bits else '')) if a.fused else 'superpose'} {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}")
+print(f"[{a.pkg or 'tree'}] {W.__file__.split('/')[-3]} {('fused' + (' no-u' if a.no_u else '') + (' no-bits' if a.no_bits else '')) if a.fused else 'superpose'} {ev[0].elapsed_time(ev[1]) / a.reps:.3f} ms for {a.rows} rows; bin entries {st['entries']}; clocks {ck}")
 if a.dump:
     import hashlib
     import numpy as np

@@ -56,7 +56,7 @@ def main():
     ap.add_argument("--depths", type=int, default=None)
     ap.add_argument("--no-d1", action="store_true")
     ap.add_argument("--path", default="auto", choices=["auto", "gather", "scatter"],
-                    help="superposition kernel (WASABI_FLAG_GATHER / _SCATTER; auto: gather iff r >= 0.6)")
+                    help="superposition kernel (WASABI_FLAG_GATHER / _SCATTER; auto: gather iff r >= 0.25)")
     ap.add_argument("--out", default="gpurun_out/c5_sweep.jsonl")
     a = ap.parse_args()
     base = CONFIGS["C5"]
@@ -106,7 +106,7 @@ def main():
             acc = W.count_accumulations(p, pl.tables, d_pts, 0, p.n_h, s8)
             st = W.bins_stats(pl.bins)
             rec = {"n_points": n, "retention": r, "aligned": a.aligned, "exact": a.exact, "wavelet": a.wavelet,
-                   "path": a.path if a.path != "auto" else ("gather" if r >= 0.6 and a.wavelet == 0 else "scatter"),
+                   "path": a.path if a.path != "auto" else ("gather" if r >= 0.25 and a.wavelet == 0 else "scatter"),
                    "levels": cfg.levels, "n_depth": cfg.n_depth, "wasabi_ms": t_w,
                    "gpix_per_s": p.n_h ** 2 / (t_w * 1e-3) / 1e9, "points_per_s": n / (t_w * 1e-3),
                    "fused_kernel_ms": t_k, "accumulations": acc,
