@@ -366,7 +366,7 @@ def run_ours(args, cfg):
            "inverse_quantize": 16.125 * rows * cfg.n_h,
            "superpose_inverse_quantize": 8.125 * rows * cfg.n_h + 16.0 * st["n_valid"],
            "bin": 16.0 * n + 16.0 * st["n_valid"] + 8.0 * st["entries"],
-           "tables": 0.0}
+           "tables": float(tb)}      # the table buffer the build writes (canonical + window LUT)
     dom = max(stage_ms, key=stage_ms.get)
     traffic, onchip = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
