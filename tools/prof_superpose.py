@@ -27,6 +27,7 @@ ap.add_argument("--path", default="auto", choices=["auto", "gather", "scatter"])
 ap.add_argument("--sort-depth", action="store_true", help="experiment: permute the points by depth (stable)")
 ap.add_argument("--no-u", action="store_true", help="fused: bits only (no u write)")
 ap.add_argument("--no-bits", action="store_true", help="fused: u only (no binarisation)")
+ap.add_argument("--snap-y", type=int, default=0, help="experiment: snap every point's pixel row to a multiple of K")
 ap.add_argument("--dump", default=None, help="np.save psi (after the timed superposes) to this path")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
@@ -36,6 +37,10 @@ if a.retention:
     cfg = cfg.replace(retention=a.retention)
 p = W.Params.from_config(cfg, path=a.path)
 pts = make_points(cfg, n=a.n)
+if a.snap_y:
+    import numpy as np
+    iy = np.floor(pts[:, 1].astype(np.float64) / cfg.pitch + 0.5)
+    pts[:, 1] = (np.round(iy / a.snap_y) * a.snap_y * cfg.pitch).astype(np.float32)
 if a.sort_depth:
     import numpy as np
     pts = pts[np.argsort(pts[:, 2], kind="stable")]
