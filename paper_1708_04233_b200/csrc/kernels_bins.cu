@@ -114,17 +114,32 @@ __global__ void __launch_bounds__(256) convert_count_kernel(const float4 *__rest
     }
 }
 
+// cursor mode (every bin position < 2^32): fill[t] starts at ptr[t] (init_cursor_kernel) and the
+// atomic returns the entry's absolute position -- no per-pair load of ptr[t]
 __global__ void __launch_bounds__(256) scatter_kernel(BinArgs A, const KDesc *__restrict__ kd,
                                                       const int4 *__restrict__ pconv,
                                                       const unsigned long long *__restrict__ ptr,
-                                                      uint32_t *__restrict__ fill, uint32_t *__restrict__ idx) {
+                                                      uint32_t *__restrict__ fill, uint32_t *__restrict__ idx,
+                                                      int cursor) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int4 q = j < A.n ? pconv[j] : make_int4(0, 0, -1, 0);
     const int64_t j0 = j - (threadIdx.x & 31);           // point index of lane 0
-    warp_footprint(q, q.z >= 0, kd, A, threadIdx.x & 31, [&](int64_t t, int src) {
-        const uint32_t slot = atomicAdd(&fill[t], 1u);
-        idx[ptr[t] + slot] = (uint32_t)(j0 + src);
-    });
+    if (cursor) {
+        warp_footprint(q, q.z >= 0, kd, A, threadIdx.x & 31, [&](int64_t t, int src) {
+            idx[atomicAdd(&fill[t], 1u)] = (uint32_t)(j0 + src);
+        });
+    } else {
+        warp_footprint(q, q.z >= 0, kd, A, threadIdx.x & 31, [&](int64_t t, int src) {
+            const uint32_t slot = atomicAdd(&fill[t], 1u);
+            idx[ptr[t] + slot] = (uint32_t)(j0 + src);
+        });
+    }
+}
+
+__global__ void __launch_bounds__(256) init_cursor_kernel(const unsigned long long *__restrict__ ptr,
+                                                          uint32_t *__restrict__ cur, int64_t n) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) cur[t] = (uint32_t)ptr[t];
 }
 
 // Warp-per-tile bitonic sort for bins of <= 1024 entries, in registers: element i = 32 e + lane
@@ -389,10 +404,16 @@ cudaError_t launch_bin(const BinHeader &h, void *d_bins, const KDesc *kd, const 
         convert_count_kernel<<<pb, 256, 0, s>>>(pts, A, kd, pconv, cnt, bh);
     }
     if ((e = launch_scan_u32_to_u64(cnt, ptr, h.n_tiles + 1, scan_scratch, s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(h.n_tiles + 1), s)) != cudaSuccess) return e;
+    const int cursor = h.capacity < (int64_t)0xffffffffLL;   // every bin position fits the 32-bit cursor
+    if (cursor) {
+        count_launches(1);
+        init_cursor_kernel<<<(unsigned)((h.n_tiles + 1 + 255) / 256), 256, 0, s>>>(ptr, cnt, h.n_tiles + 1);
+    } else if ((e = cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)(h.n_tiles + 1), s)) != cudaSuccess) {
+        return e;
+    }
     if (h.n_points > 0) {
         count_launches(1);
-        scatter_kernel<<<pb, 256, 0, s>>>(A, kd, pconv, ptr, cnt, idx);
+        scatter_kernel<<<pb, 256, 0, s>>>(A, kd, pconv, ptr, cnt, idx, cursor);
     }
     count_launches(1);
     sort_small_kernel<<<(unsigned)((h.n_tiles + 7) / 8), 256, 0, s>>>(h.n_tiles, ptr, idx, big_list, big_count);
