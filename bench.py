@@ -461,7 +461,7 @@ def run_ours(args, cfg):
                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                "data": "synthetic (seeded generators, inputs/; the paper's 3D model is unavailable)",
                "config": {"workload": _workload(cfg, args.wavelet),
-                          "path": ("unfused (coif1 halo band + line synthesis)" if args.wavelet else "unfused")
+                          "path": ("superpose on the coif1 halo band, then fused coif1 tile synthesis + quantise (u written)" if args.wavelet else "unfused")
                           if args.unfused else "fused",
                           "n_h": cfg.n_h, "n_points": n, "levels": cfg.levels, "retention": cfg.retention,
                           "n_depth": cfg.n_depth, "tile": p.tile, "rows_per_gpu": rows,

@@ -187,9 +187,13 @@ wasabi_status wasabi_superpose_inverse(const wasabi_params *params, const void *
  * coiflet mode (below).  d_u == NULL: u is not written (print only).
  * d_bits != NULL fuses step 4 (see wasabi_quantize) and requires `print`.
  * WASABI_FLAG_COIFLET: d_psi is the halo band [max(0, row0 - H), min(n_h, row1 + H)) x n_h
- * (H = wasabi_coif_halo_rows), synthesised IN PLACE (coif1, zero outside the band and the
- * hologram); rows [row0, row1) of the result are u.  d_u (rows [row0, row1)) may be NULL, may be
- * the matching row of d_psi (no copy), or another buffer (copied). */
+ * (H = wasabi_coif_halo_rows); coif1 synthesis with zero outside the band and the hologram.
+ *  - d_u outside d_psi, or d_u == NULL with d_bits: FUSED -- each 64 x 64 tile of u is synthesised
+ *    from its psi (plus a halo of 3 (2^L - 1) pixels, rounded up to 2^L) in shared memory and
+ *    quantised there; d_psi is only read.
+ *  - d_u == the matching rows of d_psi, or d_u == d_bits == NULL: the line passes run IN PLACE on
+ *    the halo band and rows [row0, row1) of d_psi are u (then d_bits, if any, from them).
+ *  Both give bit-identical u and bits. */
 wasabi_status wasabi_inverse_wt(const wasabi_params *params, float *d_psi, float *d_u, int64_t row0,
                                 int64_t row1, const wasabi_print_params *print, uint8_t *d_bits,
                                 cudaStream_t stream);

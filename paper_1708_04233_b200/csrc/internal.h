@@ -181,6 +181,8 @@ cudaError_t launch_coif_tables(const TableHeader &h, const void *d_tables, doubl
                                int64_t n_coef, double k, double pitch, int L, cudaStream_t s);
 // coif1 synthesis of a psi band (nrows x n_h) in place, levels L..1
 cudaError_t launch_coif_inverse(float2 *psi, int64_t nrows, int64_t n_h, int L, cudaStream_t s);
+cudaError_t launch_coif_fused(const float2 *psi, int64_t e0, int64_t e1, int64_t row0, int64_t row1, int64_t n_h,
+                              int L, const double *print4, double pitch, float2 *u, uint8_t *bits, cudaStream_t s);
 // gather mode: every kept canonical entry written into its table's dense copy (zeroed beforehand)
 cudaError_t launch_dense_fill(const TableHeader &h, void *d_tables, cudaStream_t s);
 cudaError_t launch_scan_i32(int32_t *data, int64_t n, void *scratch, cudaStream_t s);

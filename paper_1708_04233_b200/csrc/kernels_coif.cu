@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "internal.h"
+#include "device_common.cuh"
 
 namespace wasabi {
 namespace {
@@ -202,6 +203,180 @@ __global__ void __launch_bounds__(256) fb_inv_rows_kernel(float2 *__restrict__ p
     }
 }
 
+// ---- fused coif1 synthesis + quantise, one 64 x 64 output tile per CTA (psi read once) ----
+// The tile's psi is loaded with a halo of a_L pixels per side into shared memory (row pitch R + 1
+// cells, odd: conflict-free along rows and columns), zero outside the psi band and the hologram (the
+// R-A21 boundary, as the line passes).  Level l = L..1 (grid s = 2^(l-1)) runs its column pass then
+// its row pass in place over the square [-a_l, 64 + a_l), a_L = 3 (2^L - 1) rounded up to 2^L and
+// a_(l-1) = a_l - 3 s rounded down to 2^(l-1): an output sample depends on the samples within
+// [-2 s, +3 s], so after level 1 the square [-3, 67) is exact.  Lines are split into segments of
+// pairs, one per thread; a thread reads its neighbours' boundary pairs before a barrier and then rolls
+// along its segment (old values of pairs p - 1, p, p + 1 in registers), so the in-place passes have no
+// races.  Every output sample is computed with synth()'s operation sequence from the same inputs as
+// fb_inv_cols/rows_kernel: u and the bits are bit-identical to the line passes + quantize_kernel.
+constexpr int kCT = 64;        // output tile side
+constexpr int kCThreads = 256;
+
+__host__ __device__ inline int coif_halo(int L) {              // a_L
+    const int need = 3 * ((1 << L) - 1), g = 1 << L;
+    return (need + g - 1) / g * g;
+}
+
+// a_l of level l for an L-level synthesis: a_L = coif_halo(L), a_(l-1) = a_l - 3 s_l rounded down to
+// a multiple of 2^(l-1) (the next level's pair size)
+__host__ __device__ constexpr int coif_a(int L, int l) {
+    int a = (3 * ((1 << L) - 1) + (1 << L) - 1) / (1 << L) * (1 << L);
+    for (int k = L; k > l; k--) a = (a - 3 * (1 << (k - 1))) / (1 << (k - 1)) * (1 << (k - 1));
+    return a;
+}
+__host__ __device__ constexpr int coif_seg(int nl, int np) {   // segments per line: lines x seg <= threads
+    int seg = 1;
+    while (nl * (seg + 1) <= kCThreads && seg + 1 <= np) seg++;
+    return seg;
+}
+
+// One synthesis pass of level l (grid S = 2^(l-1)) over the square [-A, 64 + A): PASS 0 = columns
+// (lines are columns, samples along y), 1 = rows.  reg: the region, origin (-HP, -HP), pitch P cells.
+// Thread -> (line j = tid % nl, segment g = tid / nl): a warp's lanes work on adjacent lines at the
+// same sample (conflict-free shared accesses at S = 1).  Samples outside [vlo, vhi) along the line,
+// and lines outside [llo, lhi), are never written (R-A21 zeros).
+template <int PASS, int S, int A, int HP, int P>
+__device__ __forceinline__ void coif_pass(float2 *reg, const float *h0, const float *h1, int vlo, int vhi, int llo,
+                                          int lhi) {
+    constexpr int nl = (kCT + 2 * A) / S, np = nl / 2;
+    constexpr int seg = coif_seg(nl, np), per = (np + seg - 1) / seg;
+    const int tid = threadIdx.x;
+    const bool active = tid < nl * seg;
+    const int j = tid % nl, g = tid / nl;
+    const int p_beg = g * per, p_end = active ? min(np, p_beg + per) : 0;
+    const int across = -A + S * j;
+    // sample n of the line: base[n * st]
+    constexpr int st = PASS == 0 ? S * P : S;
+    float2 *base = PASS == 0 ? reg + (HP - A) * P + (across + HP) : reg + (across + HP) * P + (HP - A);
+    // writable samples n in [nlo, nhi): along-line coordinate -A + S n in [vlo, vhi), line inside [llo, lhi)
+    int nlo = 0, nhi = 0;
+    if (across >= llo && across < lhi) {
+        nlo = max(0, (vlo + A + S - 1) / S);
+        nhi = min(nl, (vhi + A + S - 1) / S);
+    }
+    const float2 z = make_float2(0.f, 0.f);
+    float2 lA = z, lD = z, rA = z, rD = z;   // old pairs p_beg - 1 and p_end (zero beyond the square)
+    if (p_beg < p_end) {
+        if (p_beg > 0) { lA = base[(2 * p_beg - 2) * st]; lD = base[(2 * p_beg - 1) * st]; }
+        if (p_end < np) { rA = base[(2 * p_end) * st]; rD = base[(2 * p_end + 1) * st]; }
+    }
+    __syncthreads();
+    if (p_beg < p_end) {
+        float2 *q = base + 2 * p_beg * st;                    // pair p
+        float2 A0 = lA, D0 = lD;                              // pair p - 1 (old)
+        float2 A1 = q[0], D1 = q[st];                         // pair p (old)
+        const bool all = nlo <= 2 * p_beg && 2 * p_end <= nhi;
+        for (int p = p_beg; p < p_end; p++, q += 2 * st) {
+            float2 A2 = rA, D2 = rD;                          // pair p + 1 (old)
+            if (p + 1 < p_end) { A2 = q[2 * st]; D2 = q[3 * st]; }
+            float2 o[2];
+#pragma unroll
+            for (int odd = 0; odd < 2; odd++) {               // synth(): k = 4 - 2 t + odd, t = 0..2
+                float2 x = z;
+                const float2 As[3] = {A0, A1, A2}, Ds[3] = {D0, D1, D2};
+#pragma unroll
+                for (int t = 0; t < 3; t++) {
+                    const int k = 4 - 2 * t + odd;
+                    x.x = fmaf(h0[k], As[t].x, fmaf(h1[k], Ds[t].x, x.x));
+                    x.y = fmaf(h0[k], As[t].y, fmaf(h1[k], Ds[t].y, x.y));
+                }
+                o[odd] = x;
+            }
+            if (all) {
+                q[0] = o[0];
+                q[st] = o[1];
+            } else {
+                if (2 * p >= nlo && 2 * p < nhi) q[0] = o[0];
+                if (2 * p + 1 >= nlo && 2 * p + 1 < nhi) q[st] = o[1];
+            }
+            A0 = A1; D0 = D1; A1 = A2; D1 = D2;
+        }
+    }
+    __syncthreads();
+}
+
+template <int L, int l>
+__device__ __forceinline__ void coif_levels(float2 *reg, const float *h0, const float *h1, int ylo, int yhi, int xlo,
+                                            int xhi) {
+    constexpr int HP = coif_a(L, L), P = kCT + 2 * HP + 1, A = coif_a(L, l), S = 1 << (l - 1);
+    coif_pass<0, S, A, HP, P>(reg, h0, h1, ylo, yhi, xlo, xhi);
+    coif_pass<1, S, A, HP, P>(reg, h0, h1, xlo, xhi, ylo, yhi);
+    if constexpr (l > 1) coif_levels<L, l - 1>(reg, h0, h1, ylo, yhi, xlo, xhi);
+}
+
+template <int L>
+__global__ void __launch_bounds__(kCThreads) coif_synth_tile_kernel(const float2 *__restrict__ psi, int64_t e0,
+                                                                    int64_t e1, int64_t row0, int64_t n_h, Filt F,
+                                                                    QArgs qa, float2 *__restrict__ u,
+                                                                    uint8_t *__restrict__ bits) {
+    extern __shared__ float2 reg[];
+    constexpr int hp = coif_a(L, L), R = kCT + 2 * hp, P = R + 1;
+    static_assert(hp == coif_a(L, L) && coif_a(L, 1) >= 3, "coif1 halo");
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int tiles_x = (int)(n_h / kCT);
+    const int64_t tile_x0 = (int64_t)(blockIdx.x % tiles_x) * kCT;
+    const int64_t tile_y0 = row0 + (int64_t)(blockIdx.x / tiles_x) * kCT;
+    float h0[6], h1[6];
+#pragma unroll
+    for (int k = 0; k < 6; k++) { h0[k] = (float)F.h0[k]; h1[k] = (float)F.h1[k]; }
+    // R-A21 boundary: samples outside the psi band rows [e0, e1) and the hologram columns are zero at
+    // every level (as in the line passes, whose lines end there): loaded as zero, never written
+    const int ylo = (int)max((int64_t)-hp, e0 - tile_y0), yhi = (int)min((int64_t)(kCT + hp), e1 - tile_y0);
+    const int xlo = (int)max((int64_t)-hp, -tile_x0), xhi = (int)min((int64_t)(kCT + hp), n_h - tile_x0);
+    // load (asynchronous 8-byte copies, zero-filled outside): a warp per region row
+    const uint32_t rsa = (uint32_t)__cvta_generic_to_shared(reg);
+    if (ylo == -hp && yhi == kCT + hp && xlo == -hp && xhi == kCT + hp) {   // interior tile: no checks
+        const float2 *src = psi + (tile_y0 - hp - e0) * n_h + tile_x0 - hp + lane;
+        for (int y = tid >> 5; y < R; y += kCThreads / 32) {
+            uint32_t dst = rsa + 8u * (uint32_t)(y * P + lane);
+            const float2 *sr = src + (int64_t)y * n_h;
+#pragma unroll
+            for (int x = 0; x < R; x += 32, dst += 256u)
+                if (x + lane < R) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(sr + x) : "memory");
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    } else {
+        for (int y = (tid >> 5) - hp; y < kCT + hp; y += kCThreads / 32) {
+            const bool rok = y >= ylo && y < yhi;
+            const float2 *src = psi + (tile_y0 + y - e0) * n_h + tile_x0;
+            uint32_t dst = rsa + 8u * (uint32_t)((y + hp) * P + lane);
+            for (int x = lane - hp; x < kCT + hp; x += 32, dst += 256u) {
+                const bool ok = rok && x >= xlo && x < xhi;
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(ok ? src + x : psi),
+                             "r"(ok ? 8 : 0) : "memory");
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
+    coif_levels<L, L>(reg, h0, h1, ylo, yhi, xlo, xhi);
+    // step 4 on the tile (same print_byte as quantize_kernel) and the u write
+    auto cell = [&](int y, int x) -> const float2 & { return reg[(y + hp) * P + (x + hp)]; };
+    if (bits) {
+        for (int b = tid; b < kCT * (kCT / 8); b += kCThreads) {   // lanes on adjacent rows: no bank conflicts
+            const int y = b % kCT, xb = b / kCT;
+            float2 v[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) v[i] = cell(y, xb * 8 + i);
+            const int64_t Y = tile_y0 + y;
+            bits[(Y - row0) * (n_h / 8) + tile_x0 / 8 + xb] = (uint8_t)print_byte(v, tile_x0 + xb * 8, ref_row(Y, qa), qa);
+        }
+    }
+    if (u) {
+        float2 *out = u + (tile_y0 - row0) * n_h + tile_x0;
+        for (int y = tid >> 5; y < kCT; y += kCThreads / 32) {
+            __stcs(out + y * n_h + lane, cell(y, lane));
+            __stcs(out + y * n_h + lane + 32, cell(y, lane + 32));
+        }
+    }
+}
+
 }  // namespace
 
 // coif1 (R-A21): h0 = sqrt(2)/32 [1-s, 5+s, 14+2s, 14-2s, 1-s, -3+s], s = sqrt(7); h1[k] = (-1)^k h0[5-k].
@@ -249,4 +424,32 @@ cudaError_t launch_coif_inverse(float2 *psi, int64_t nrows, int64_t n_h, int L, 
     return cudaGetLastError();
 }
 
+}  // namespace wasabi
+
+namespace wasabi {
+// Fused coif1 synthesis + quantise of band [row0, row1) from the halo band psi [e0, e1) (read only).
+cudaError_t launch_coif_fused(const float2 *psi, int64_t e0, int64_t e1, int64_t row0, int64_t row1, int64_t n_h,
+                              int L, const double *print4, double pitch, float2 *u, uint8_t *bits, cudaStream_t s) {
+    const Filt F = coif1();
+    const QArgs qa = make_qargs(print4, pitch, n_h);
+    const int hp = coif_halo(L), R = kCT + 2 * hp;
+    const int smem = R * (R + 1) * (int)sizeof(float2);
+    const int64_t tiles = (n_h / kCT) * ((row1 - row0) / kCT);
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        if (tiles > 0) {
+            count_launches(1);
+            kern<<<(unsigned)tiles, kCThreads, smem, s>>>(psi, e0, e1, row0, n_h, F, qa, u, bits);
+        }
+        return cudaGetLastError();
+    };
+    switch (L) {
+        case 1: return go(coif_synth_tile_kernel<1>);
+        case 2: return go(coif_synth_tile_kernel<2>);
+        case 3: return go(coif_synth_tile_kernel<3>);
+        case 4: return go(coif_synth_tile_kernel<4>);
+        default: return cudaErrorInvalidValue;
+    }
+}
 }  // namespace wasabi

@@ -639,7 +639,17 @@ wasabi_status wasabi_inverse_wt(const wasabi_params *params, float *d_psi, float
     if (params->flags & WASABI_FLAG_COIFLET) {   // R-A21: in place on the halo band, then u rows, then bits
         const int64_t H = wasabi_coif_halo_rows(params);
         const int64_t e0 = std::max<int64_t>(0, row0 - H), e1 = std::min<int64_t>(params->n_h, row1 + H);
-        float2 *pe = reinterpret_cast<float2 *>(d_psi);   // coiflets: synthesised in place (wasabi.h)
+        float2 *pe = reinterpret_cast<float2 *>(d_psi);
+        const float2 *u2 = reinterpret_cast<const float2 *>(d_u);
+        const bool u_in_psi = d_u && u2 < pe + (e1 - e0) * params->n_h && u2 + (row1 - row0) * params->n_h > pe;
+        if ((d_u || d_bits) && !u_in_psi) {   // fused tile synthesis + quantise; d_psi is only read (wasabi.h)
+            if (row1 > row0)
+                CK(launch_coif_fused(pe, e0, e1, row0, row1, params->n_h, params->levels, print ? p4 : nullptr,
+                                     params->pitch_m, reinterpret_cast<float2 *>(d_u), d_bits, stream),
+                   "coif fused inverse");
+            return WASABI_OK;
+        }
+        // line passes in place on the halo band (wasabi.h)
         if (e1 > e0) CK(launch_coif_inverse(pe, e1 - e0, params->n_h, params->levels, stream), "coif inverse");
         float2 *uc = pe + (row0 - e0) * params->n_h;
         if (d_u && reinterpret_cast<float2 *>(d_u) != uc && row1 > row0)
@@ -847,8 +857,11 @@ wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_pri
     const size_t bpr = (size_t)(params->n_h / 8), upr = 8 * (size_t)params->n_h;   // bytes per row
     if (params->flags & WASABI_FLAG_COIFLET) {   // unfused: psi on the halo band, coif1 synthesis, bits
         if ((st = wasabi_superpose(params, ws + w.tables, ws + w.bins, w.e0, w.e1, d_field, stream))) return st;
-        if ((st = wasabi_inverse_wt(params, d_field, nullptr, row0, row1, print, d_bits, stream))) return st;
-        d_field += 2 * (row0 - w.e0) * params->n_h;   // u rows [row0, row1) inside the halo band
+        // with u wanted: in place on the halo band (u = its rows [row0, row1)); print only: fused tiles
+        float *d_urows = d_field + 2 * (row0 - w.e0) * params->n_h;   // u rows [row0, row1) inside the halo band
+        if ((st = wasabi_inverse_wt(params, d_field, h_u ? d_urows : nullptr, row0, row1, print, d_bits, stream)))
+            return st;
+        d_field = d_urows;
         CK(join(cs, stream), "wait for u");
         if (h_bits && row1 > row0)
             CK(cudaMemcpyAsync(h_bits, d_bits, bpr * (size_t)(row1 - row0), cudaMemcpyDeviceToHost, cs), "D2H bits");

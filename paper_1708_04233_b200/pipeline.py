@@ -38,11 +38,14 @@ class Pipeline:
         self.bins = torch.empty(bin_points_bytes(p, n_max, self.e0, self.e1), dtype=torch.uint8,
                                 device=self.device)
         rows = self.row1 - self.row0
-        if self.e0 == self.row0 and self.e1 == self.row1:
+        if p.wavelet == 0:
             self.psi_band = self.field = torch.empty((rows, p.n_h, 2), dtype=torch.float32, device=self.device)
         else:
+            # coiflets: psi on the halo band; u in its own buffer, so wasabi_inverse_wt runs the fused tile
+            # synthesis (psi only read).  Print only (want_u False): field is a view of psi's band rows.
             self.psi_band = torch.empty((self.e1 - self.e0, p.n_h, 2), dtype=torch.float32, device=self.device)
-            self.field = self.psi_band[self.row0 - self.e0:self.row1 - self.e0]   # u rows (a view)
+            self.field = (torch.empty((rows, p.n_h, 2), dtype=torch.float32, device=self.device) if want_u
+                          else self.psi_band[self.row0 - self.e0:self.row1 - self.e0])
         self.bits = torch.empty((rows, p.n_h // 8), dtype=torch.uint8, device=self.device) if want_bits else None
         self.want_u = want_u
         self.stream = stream

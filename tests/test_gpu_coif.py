@@ -94,6 +94,40 @@ def test_coif_hologram_host_equals_device_path(W):
     assert np.array_equal(hu[..., 0] + 1j * hu[..., 1], u_g.astype(np.complex64).astype(np.complex128))
 
 
+@pytest.mark.parametrize("name,row0,row1,kw", [("C1", 0, 512, {}), ("C1", 192, 384, dict(levels=4)),
+                                             ("C1", 128, 448, dict(levels=1)), ("C1", 64, 320, dict(levels=2)),
+                                             ("C2", 1024, 1536, dict(levels=3, retention=0.05)),
+                                             ("C1", 128, 384, dict(tile=128))])
+def test_coif_fused_tiles_equal_line_passes(W, name, row0, row1, kw):
+    """wasabi_inverse_wt in coiflet mode: the fused tile synthesis + quantise (u in its own buffer,
+    psi only read) is bit-identical to the in-place line passes + quantize_kernel (u = psi's band
+    rows), for L = 1..4, bands inside and at the hologram edges, and tile 128 bins."""
+    import torch
+    cfg = CONFIGS[name].replace(**kw)
+    pts = make_points(cfg, n=3000 if name == "C2" else None)
+    p = gpu_params(cfg, wavelet=1)
+    pl = W.Pipeline(p, len(pts), row0, row1)
+    pl.build_tables()
+    pl.bin(torch.from_numpy(pts).cuda())
+    pl.superpose()
+    psi = pl.psi_band.clone()
+    rows = row1 - row0
+    u_f = torch.empty((rows, p.n_h, 2), dtype=torch.float32, device="cuda")
+    b_f = torch.empty((rows, p.n_h // 8), dtype=torch.uint8, device="cuda")
+    W.inverse_wt(p, pl.psi_band, u_f, row0, row1, W.PrintParams(), b_f)          # fused
+    b_p = torch.empty_like(b_f)
+    W.inverse_wt(p, pl.psi_band, None, row0, row1, W.PrintParams(), b_p)         # fused, print only
+    torch.cuda.synchronize()
+    assert torch.equal(pl.psi_band, psi), "the fused path must not write psi"
+    b_l = torch.empty_like(b_f)
+    u_l = pl.psi_band[row0 - pl.e0:row1 - pl.e0]
+    W.inverse_wt(p, pl.psi_band, u_l, row0, row1, W.PrintParams(), b_l)          # line passes in place
+    torch.cuda.synchronize()
+    assert torch.equal(u_f, u_l), float((u_f - u_l).abs().max())
+    assert torch.equal(b_f, b_l) and torch.equal(b_p, b_l)
+    assert float(u_f.abs().max()) > 0
+
+
 def test_coif_fused_entry_refuses(W):
     import torch
     cfg = CONFIGS["C1"]

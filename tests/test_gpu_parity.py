@@ -100,7 +100,7 @@ def _gpu_run(W, cfg, pts, row0, row1, **kw):
     pl.build_tables()
     pl.bin(d_pts)
     pl.superpose()
-    psi = field_np(pl.field)
+    psi = field_np(pl.psi_band[row0 - pl.e0:row1 - pl.e0])   # == pl.field unless coiflets (halo band)
     pl.inverse()
     torch.cuda.synchronize()
     return pl, psi, field_np(pl.field), pl.bits.cpu().numpy()
