@@ -18,7 +18,7 @@ __host__ __device__ inline uint32_t pack_entry_pos(int X, int Y, int level) {
     return (uint32_t)X | ((uint32_t)Y << 14) | ((uint32_t)level << 28);
 }
 
-// Compact per-table data read by the hot kernels (80 bytes).
+// Compact per-table data read by the hot kernels (112 bytes).
 struct KDesc {
     int32_t H;                    // table half side (H, vbase: one 8-byte load in the hot kernel)
     int32_t vbase;                // window LUT pointer slots of this table start here (== vptr_base[0])
@@ -30,8 +30,16 @@ struct KDesc {
     int32_t side;                 // table side: 2H, or 2H + 2^L for offset-class tables (R-A20)
     int32_t Ed;                   // PSF-disc reach per axis, ceil(Rh), Rh = R(|z_d| + dz/2) + 1 (direct sums)
     int32_t Qd;                   // PSF-disc reach, squared distance ceil(Rh^2)
-};
-static_assert(sizeof(KDesc) % 8 == 0, "KDesc: (H, vbase) is read as one 8-byte load");
+    int32_t cls4[2][4];           // superposition warp class c: {H, vptr_base of its level slots 0..2}
+};                                // (one 16-byte load per point; superpose_class_level)
+static_assert(sizeof(KDesc) % 16 == 0 && offsetof(KDesc, cls4) % 16 == 0, "KDesc: cls4[c] is one 16-byte load");
+
+// Level of slot j (0..2) of superposition warp class c (every Haar level owns its own pixels, R-A6):
+// c = 0 -> {1, 3, 6}, c = 1 -> {2, 4, 5}; 0 = none (levels beyond L).
+__host__ __device__ inline int superpose_class_level(int c, int j, int L) {
+    const int l = c == 0 ? (j == 0 ? 1 : j == 1 ? 3 : j == 2 ? 6 : 0) : (j == 0 ? 2 : j < 3 ? j + 3 : 0);
+    return l <= L ? l : 0;
+}
 
 // Offset-class tables (WASABI_FLAG_EXACT_SHIFT, reading R-A20): with cb = L class bits, depth d
 // has 4^L tables t = (d << 2cb) | (cy << cb) | cx, (cx, cy) = (ix, iy) mod 2^L; every level of a

@@ -88,7 +88,10 @@ __global__ void __launch_bounds__(256) fb_fwd_pass_kernel(const void *tables, co
     const DDesc D = dd[t];
     const int side = D.side, s = 1 << (l - 1), N = side >> (l - 1);
     const int64_t local = g - pre[t];
-    const int j = (int)(local / (N / 2)), m = (int)(local % (N / 2));
+    // rows: adjacent threads take adjacent pairs of a row; columns: adjacent columns at the same pair
+    // (coalesced along the row in both cases)
+    const int j = rows ? (int)(local / (N / 2)) : (int)(local % N);
+    const int m = rows ? (int)(local % (N / 2)) : (int)(local / N);
     const double2 *in = src + D.coef_off;
     double2 *out = dst + D.coef_off;
     // sample n of line j

@@ -150,19 +150,8 @@ __device__ float4 g_zero[128 * (128 + kWinMargin + 2) / 2 + 16];   // zeros (sta
 #ifndef WASABI_STCS
 #define WASABI_STCS 1
 #endif
-#ifndef WASABI_CLS
-#define WASABI_CLS 2
-#endif
-__device__ __forceinline__ int class_level(int c, int j, int L) {
-#if WASABI_CLS == 2   // {1, 3, 6} / {2, 4, 5}: three level slots per warp
-    const int l = c == 0 ? (j == 0 ? 1 : j == 1 ? 3 : j == 2 ? 6 : 0) : (j == 0 ? 2 : j < 3 ? j + 3 : 0);
-#elif WASABI_CLS == 1   // {1, 3} / {2, 4, 5, 6}: 0.3% faster at C4 than {1, 4, 5, 6} / {2, 3}
-    const int l = c == 0 ? (j < 2 ? 2 * j + 1 : 0) : (j == 0 ? 2 : j + 3);
-#else
-    const int l = c == 0 ? (j == 0 ? 1 : j + 3) : (j < 2 ? j + 2 : 0);
-#endif
-    return l <= L ? l : 0;
-}
+// levels of class c, slot j: superpose_class_level (internal.h), c = 0 -> {1, 3, 6}, c = 1 -> {2, 4, 5};
+// the table descriptor carries, per class, H and the window-pointer rows of those levels (KDesc.cls4)
 
 // Steps 3 (+4) of a T x T psi tile held in shared memory (swizzled cells, swz), shared by the scatter
 // and gather superposition kernels: fused -> the R-A6 inverse butterflies level by level in place, the
@@ -312,8 +301,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     __syncthreads();
 #endif
 
-    const int lv0 = class_level(cls, 0, A.L), lv1 = class_level(cls, 1, A.L);
-    const int lv2 = class_level(cls, 2, A.L), lv3 = class_level(cls, 3, A.L);
+    const int lv0 = superpose_class_level(cls, 0, A.L), lv1 = superpose_class_level(cls, 1, A.L);
+    const int lv2 = superpose_class_level(cls, 2, A.L);
     const unsigned long long b1 = bptr[t + 1];
     unsigned long long pb = bptr[t];
 
@@ -321,8 +310,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     // | length; the CURRENT batch (beg, pk, a_l) and the NEXT one (nbeg, npk, na), loaded while the
     // current batch's chunks stream (software-pipelined batches, WASABI_PIPE)
     float a_l = 0.f, na = 0.f;
-    constexpr int kSlots = WASABI_CLS == 2 ? 3 : 4;   // level slots per warp
-    int beg[4] = {0, 0, 0, 0}, pk[4] = {0, 0, 0, 0}, nbeg[4] = {0, 0, 0, 0}, npk[4] = {0, 0, 0, 0};
+    constexpr int kSlots = 3;                         // level slots per warp
+    int beg[3] = {0, 0, 0}, pk[3] = {0, 0, 0}, nbeg[3] = {0, 0, 0}, npk[3] = {0, 0, 0};
     const int cb = EX ? A.L : 0;               // offset-class bits (R-A20) or 0
     const int cmask = (1 << cb) - 1;
     auto range = [&](int l, int ix, int iy, int H, int side, int vrow, bool ok, int &b, int &p) {
@@ -361,26 +350,14 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             const int4 q = qn;
             qn = pb + nq + lane < b1 ? __ldg(pconv + nidx) : make_int4(0, 0, 0, 0);
             nidx = pb + nq + 32 + lane < b1 ? __ldg(bidx + pb + nq + 32 + lane) : 0u;
-            int2 hv = make_int2(0, 0);          // (H, first window-LUT pointer slot)
-            if (ok) hv = __ldg(reinterpret_cast<const int2 *>(&kd[table_of(q.x, q.y, q.z, cb)].H));
+            int4 hv = make_int4(0, 0, 0, 0);    // (H, window-pointer rows of the class's three levels)
+            if (ok) hv = __ldg(reinterpret_cast<const int4 *>(kd[table_of(q.x, q.y, q.z, cb)].cls4[cls]));
             pb += nq;
             oa = __int_as_float(q.w);
             const int side = 2 * hv.x + (EX ? 1 << A.L : 0);
-            // pointer rows of the class's levels: level l starts after the slots of levels < l
-            int vr[4];
-            {
-                int acc = hv.y, l = 1;
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const int lj = j == 0 ? lv0 : j == 1 ? lv1 : j == 2 ? lv2 : lv3;
-                    for (; l < lj; l++) acc += win_slots(side, l, cb);
-                    vr[j] = acc;
-                }
-            }
-            range(lv0, q.x, q.y, hv.x, side, vr[0], ok, ob[0], op[0]);
-            range(lv1, q.x, q.y, hv.x, side, vr[1], ok, ob[1], op[1]);
-            range(lv2, q.x, q.y, hv.x, side, vr[2], ok, ob[2], op[2]);
-            if (kSlots > 3) range(lv3, q.x, q.y, hv.x, side, vr[3], ok, ob[3], op[3]);
+            range(lv0, q.x, q.y, hv.x, side, hv.y, ok, ob[0], op[0]);
+            range(lv1, q.x, q.y, hv.x, side, hv.z, ok, ob[1], op[1]);
+            range(lv2, q.x, q.y, hv.x, side, hv.w, ok, ob[2], op[2]);
             bool any = false;
 #pragma unroll
             for (int j = 0; j < kSlots; j++) any |= __any_sync(kFull, (op[j] & 0xffff) != 0);
@@ -397,8 +374,8 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     int have = 0, nhave = 0, refill = 0;   // ints, not bools: bools get byte-packed (PRMT per update)
     int s_beg = 0, s_pk = 0;                 // this lane's range for slot gj: first entry, (base << 16) | length
     auto select_slot = [&]() {
-        s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : (kSlots == 3 || gj == 2) ? beg[2] : beg[3];
-        s_pk = gj == 0 ? pk[0] : gj == 1 ? pk[1] : (kSlots == 3 || gj == 2) ? pk[2] : pk[3];
+        s_beg = gj == 0 ? beg[0] : gj == 1 ? beg[1] : beg[2];
+        s_pk = gj == 0 ? pk[0] : gj == 1 ? pk[1] : pk[2];
         gm = __ballot_sync(kFull, (s_pk & 0xffff) != 0);
     };
     auto next_range = [&]() {

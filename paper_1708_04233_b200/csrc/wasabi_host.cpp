@@ -271,6 +271,13 @@ wasabi_status compute_geo_uncached(const wasabi_params *P, Geo &g) {
             vptr += win_slots(D.side, l, g.cb);
         }
         for (int l = g.L + 1; l <= kMaxLevels; l++) K.vptr_base[l - 1] = (int32_t)vptr;
+        for (int c = 0; c < 2; c++) {
+            K.cls4[c][0] = (int32_t)H;
+            for (int j = 0; j < 3; j++) {
+                const int l = superpose_class_level(c, j, g.L);
+                K.cls4[c][1 + j] = l ? K.vptr_base[l - 1] : 0;
+            }
+        }
         D.nnz = g.wav ? nnz_coif(side, H, R, g.L) : nnz_structural(side, H + cx, H + cy, R, g.L);
         {
             const int64_t r_ppm = llround(P->retention * 1e6);

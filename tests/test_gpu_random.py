@@ -69,7 +69,7 @@ def test_random_problem_parity(W, orc, seed, mode):
     pl.build_tables()
     pl.bin(d[:len(pts)])
     pl.superpose()
-    psi_g = field_np(pl.field)
+    psi_g = field_np(pl.psi_band[row0 - pl.e0:row1 - pl.e0])   # == pl.field unless coiflets (halo band)
     pl.inverse()
     torch.cuda.synchronize()
     u_g = field_np(pl.field)
