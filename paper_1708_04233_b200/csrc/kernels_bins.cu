@@ -47,12 +47,14 @@ __device__ __forceinline__ bool convert_point(const float4 p, const BinArgs &A, 
 }
 
 // Tile range of a point's footprint square [ix-E, ix+E] x [iy-E, iy+E] within the band (E = Ek).
+// (T is 64 or 128, wasabi_params validation: floor division is an arithmetic shift)
 __device__ __forceinline__ void tile_range(int ix, int iy, int E, const BinArgs &A, int &tx0, int &tx1, int &ty0,
                                            int &ty1) {
-    tx0 = (int)max(0LL, floor_div((long long)ix - E, A.T));
-    tx1 = (int)min((long long)A.tiles_x - 1, floor_div((long long)ix + E, A.T));
-    ty0 = (int)max(0LL, floor_div((long long)iy - E - A.row0, A.T));
-    ty1 = (int)min((long long)A.tiles_y - 1, floor_div((long long)iy + E - A.row0, A.T));
+    const int sh = A.T == 64 ? 6 : 7;
+    tx0 = (int)max(0LL, ((long long)ix - E) >> sh);
+    tx1 = (int)min((long long)A.tiles_x - 1, ((long long)ix + E) >> sh);
+    ty0 = (int)max(0LL, ((long long)iy - E - A.row0) >> sh);
+    ty1 = (int)min((long long)A.tiles_y - 1, ((long long)iy + E - A.row0) >> sh);
 }
 
 // Squared distance from coordinate i to the tile span [t0, t0 + T - 1] along one axis (0 inside).
@@ -83,10 +85,16 @@ __device__ __forceinline__ void warp_footprint(int4 q, bool valid, const KDesc *
         const int w = tx1 - tx0 + 1, hgt = ty1 - ty0 + 1;
         if (w <= 0 || hgt <= 0) continue;              // footprint entirely outside the band
         const int nbox = w * hgt;
+        // box cell i = lane + 32 k -> (row i / w, column i % w), stepped without a division per cell
+        const int q32 = 32 / w, r32 = 32 - q32 * w;
+        int qy = lane / w, rx = lane - qy * w;
         for (int i = lane; i < nbox; i += 32) {
-            const int ty = ty0 + i / w, tx = tx0 + i % w;
+            const int ty = ty0 + qy, tx = tx0 + rx;
             const int rem = Q - sq_gap(iy, (int)A.row0 + ty * A.T, A.T);
             if (rem >= 0 && sq_gap(ix, tx * A.T, A.T) <= rem) f((int64_t)ty * A.tiles_x + tx, src);
+            qy += q32;
+            rx += r32;
+            if (rx >= w) { rx -= w; qy++; }
         }
     }
 }
