@@ -7,11 +7,14 @@
 //   step 1: psf_f64_kernel (PSF into an fp64 work table), fb_fwd_pass_kernel (per level: rows A->B,
 //           columns B->A, fp64, taps summed in order k = 0..5 with _rn operations -- the same IEEE
 //           sequence as the specification, so the fp32 rank keys match bit for bit), coef_keys_kernel.
-//   step 3: fb_inv_cols_kernel / fb_inv_rows_kernel: per level (L..1) columns then rows, in place on
+//   step 3 (+4): coif_synth_tile_kernel<L>: per 64 x 64 output tile, psi plus a halo in shared memory,
+//           the L levels of column and row passes in place, then the print bits and u (psi only read);
+//           or fb_inv_cols_kernel / fb_inv_rows_kernel: per level (L..1) columns then rows, in place on
 //           the psi band that carries a halo of one tile row (rolling window of pairs along the lines
-//           in shared memory; fp32).  Samples outside the band / hologram are zero (R-A21 boundary).
-// Off the fused hot path: the coiflet inverse is not block-local, so this mode runs superpose on the
-// halo band, then the line passes, then quantise.
+//           in shared memory; fp32), then quantize_kernel.  Samples outside the band / hologram are
+//           zero (R-A21 boundary); both give bit-identical u and bits.
+// The coiflet inverse is not block-local (its halo crosses tiles), so this mode superposes psi on the
+// halo band first (no superpose -> inverse fusion as in the Haar path).
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -220,13 +223,8 @@ __global__ void __launch_bounds__(256) fb_inv_rows_kernel(float2 *__restrict__ p
 constexpr int kCT = 64;        // output tile side
 constexpr int kCThreads = 256;
 
-__host__ __device__ inline int coif_halo(int L) {              // a_L
-    const int need = 3 * ((1 << L) - 1), g = 1 << L;
-    return (need + g - 1) / g * g;
-}
-
-// a_l of level l for an L-level synthesis: a_L = coif_halo(L), a_(l-1) = a_l - 3 s_l rounded down to
-// a multiple of 2^(l-1) (the next level's pair size)
+// a_l of level l for an L-level synthesis: a_L = 3 (2^L - 1) rounded up to 2^L (the halo), a_(l-1) =
+// a_l - 3 s_l rounded down to a multiple of 2^(l-1) (the next level's pair size)
 __host__ __device__ constexpr int coif_a(int L, int l) {
     int a = (3 * ((1 << L) - 1) + (1 << L) - 1) / (1 << L) * (1 << L);
     for (int k = L; k > l; k--) a = (a - 3 * (1 << (k - 1))) / (1 << (k - 1)) * (1 << (k - 1));
@@ -319,7 +317,7 @@ __global__ void __launch_bounds__(kCThreads) coif_synth_tile_kernel(const float2
                                                                     uint8_t *__restrict__ bits) {
     extern __shared__ float2 reg[];
     constexpr int hp = coif_a(L, L), R = kCT + 2 * hp, P = R + 1;
-    static_assert(hp == coif_a(L, L) && coif_a(L, 1) >= 3, "coif1 halo");
+    static_assert(coif_a(L, 1) >= 3, "coif1 halo: the square of level 1 must cover [-3, 67)");
     const int tid = threadIdx.x, lane = tid & 31;
     const int tiles_x = (int)(n_h / kCT);
     const int64_t tile_x0 = (int64_t)(blockIdx.x % tiles_x) * kCT;
@@ -435,7 +433,7 @@ cudaError_t launch_coif_fused(const float2 *psi, int64_t e0, int64_t e1, int64_t
                               int L, const double *print4, double pitch, float2 *u, uint8_t *bits, cudaStream_t s) {
     const Filt F = coif1();
     const QArgs qa = make_qargs(print4, pitch, n_h);
-    const int hp = coif_halo(L), R = kCT + 2 * hp;
+    const int hp = coif_a(L, L), R = kCT + 2 * hp;
     const int smem = R * (R + 1) * (int)sizeof(float2);
     const int64_t tiles = (n_h / kCT) * ((row1 - row0) / kCT);
     auto go = [&](auto kern) -> cudaError_t {
