@@ -221,7 +221,10 @@ __global__ void __launch_bounds__(256) fb_inv_rows_kernel(float2 *__restrict__ p
 // races.  Every output sample is computed with synth()'s operation sequence from the same inputs as
 // fb_inv_cols/rows_kernel: u and the bits are bit-identical to the line passes + quantize_kernel.
 constexpr int kCT = 64;        // output tile side
-constexpr int kCThreads = 256;
+#ifndef WASABI_COIF_THREADS
+#define WASABI_COIF_THREADS 384   // 12 warps x 2 CTAs per SM: measured best of 256..512 (2.79 -> 2.69 ms per 4096-row C4 band)
+#endif
+constexpr int kCThreads = WASABI_COIF_THREADS;
 
 // a_l of level l for an L-level synthesis: a_L = 3 (2^L - 1) rounded up to 2^L (the halo), a_(l-1) =
 // a_l - 3 s_l rounded down to a multiple of 2^(l-1) (the next level's pair size)

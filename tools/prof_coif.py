@@ -5,6 +5,9 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+for i, arg in enumerate(sys.argv):          # --pkg DIR: import the package from a variant copy
+    if arg == "--pkg":
+        sys.path.insert(0, os.path.abspath(sys.argv[i + 1]))
 import torch  # noqa: E402
 
 import paper_1708_04233_b200 as W  # noqa: E402
@@ -15,6 +18,7 @@ ap.add_argument("--row0", type=int, default=32768)
 ap.add_argument("--rows", type=int, default=4096)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--mode", default="both", choices=["both", "fused", "lines"])
+ap.add_argument("--pkg", default=None)
 a = ap.parse_args()
 cfg = CONFIGS["C4"].replace(levels=3)
 p = W.Params.from_config(cfg, wavelet=1)
