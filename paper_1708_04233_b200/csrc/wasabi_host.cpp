@@ -647,8 +647,10 @@ wasabi_status wasabi_inverse_wt(const wasabi_params *params, float *d_psi, float
         const int64_t H = wasabi_coif_halo_rows(params);
         const int64_t e0 = std::max<int64_t>(0, row0 - H), e1 = std::min<int64_t>(params->n_h, row1 + H);
         float2 *pe = reinterpret_cast<float2 *>(d_psi);
-        const float2 *u2 = reinterpret_cast<const float2 *>(d_u);
-        const bool u_in_psi = d_u && u2 < pe + (e1 - e0) * params->n_h && u2 + (row1 - row0) * params->n_h > pe;
+        // does d_u overlap the psi halo band? (address ranges compared as integers)
+        const uintptr_t ub = reinterpret_cast<uintptr_t>(d_u), pb = reinterpret_cast<uintptr_t>(d_psi);
+        const bool u_in_psi = d_u && ub < pb + 8 * (uintptr_t)((e1 - e0) * params->n_h) &&
+                              ub + 8 * (uintptr_t)((row1 - row0) * params->n_h) > pb;
         if ((d_u || d_bits) && !u_in_psi) {   // fused tile synthesis + quantise; d_psi is only read (wasabi.h)
             if (row1 > row0)
                 CK(launch_coif_fused(pe, e0, e1, row0, row1, params->n_h, params->levels, print ? p4 : nullptr,
