@@ -5,7 +5,7 @@
 //
 // Design (DESIGN.md §6 "Superpose").  One CTA owns one T x T tile of psi in shared memory and
 // walks the tile's bin (points in ascending order).  Warp w owns the pixels of level class
-// c = w & 1 ({1, 3, 6} or {2, 4, 5}; every Haar level occupies its own pixels) in the 32-row strip
+// c = w & 1 ({1, 3, 6} or {2, 4, 5}; {1} or {2, 3} for L <= 3; every level has its own pixels) in the 32-row strip
 // w >> 1, so the warps of a CTA accumulate concurrently without atomics.  For a point and a level
 // of its class, the kept coefficients landing in the strip are ONE contiguous range of the window
 // LUT (internal.h: per-variant 32-row bands, column-group pointers), so a batch of 32 points
@@ -134,7 +134,6 @@ __device__ __forceinline__ void sts2(uint32_t a, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
 
-// levels of class c, slot j (0 = none): c = 0 -> {1, 3, 6}, c = 1 -> {2, 4, 5}
 #ifndef WASABI_DEBUG_BOUNDS
 #define WASABI_DEBUG_BOUNDS 0   // 1: trap on a shared access outside the tile or a LUT index outside the arrays
 #endif
@@ -150,7 +149,7 @@ __device__ float4 g_zero[128 * (128 + kWinMargin + 2) / 2 + 16];   // zeros (sta
 #ifndef WASABI_STCS
 #define WASABI_STCS 1
 #endif
-// levels of class c, slot j: superpose_class_level (internal.h), c = 0 -> {1, 3, 6}, c = 1 -> {2, 4, 5};
+// levels of class c, slot j: superpose_class_level (internal.h), c = 0 -> {1, 3, 6}, c = 1 -> {2, 4, 5} (L <= 3: {1} / {2, 3});
 // the table descriptor carries, per class, H and the window-pointer rows of those levels (KDesc.cls4)
 
 // Steps 3 (+4) of a T x T psi tile held in shared memory (swizzled cells, swz), shared by the scatter

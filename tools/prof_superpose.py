@@ -24,6 +24,8 @@ ap.add_argument("--pkg", default=None)
 ap.add_argument("--retention", type=float, default=None)
 ap.add_argument("--n", type=int, default=None, help="point count (default: the config's)")
 ap.add_argument("--path", default="auto", choices=["auto", "gather", "scatter"])
+ap.add_argument("--wavelet", type=int, default=0, help="1: coif1 tables (superpose on the psi band, unfused)")
+ap.add_argument("--levels", type=int, default=None)
 ap.add_argument("--sort-depth", action="store_true", help="experiment: permute the points by depth (stable)")
 ap.add_argument("--no-u", action="store_true", help="fused: bits only (no u write)")
 ap.add_argument("--no-bits", action="store_true", help="fused: u only (no binarisation)")
@@ -35,7 +37,9 @@ if a.tile:
     cfg = cfg.replace(tile=a.tile)
 if a.retention:
     cfg = cfg.replace(retention=a.retention)
-p = W.Params.from_config(cfg, path=a.path)
+if a.levels:
+    cfg = cfg.replace(levels=a.levels)
+p = W.Params.from_config(cfg, path=a.path, wavelet=a.wavelet)
 pts = make_points(cfg, n=a.n)
 if a.snap_y:
     import numpy as np
