@@ -148,20 +148,40 @@ __global__ void __launch_bounds__(256) select_hist_kernel(const void *tables, co
     if (c) atomicAdd(&hist[d * 256 + threadIdx.x], c);
 }
 
-// K2b: per depth, choose the digit containing the k-th largest key; zero the histogram.
+// K2b: per depth (one warp), choose the digit containing the k-th largest key; zero the histogram.
+// Lane t holds digits 255 - 8 t .. 248 - 8 t (descending); a warp scan of the lane sums finds the lane
+// whose digits reach the k-th key, that lane scans its own 8: digit b = the largest with
+// sum(hist[b..255]) >= k, as the serial scan from 255 down.
 __global__ void select_pick_kernel(unsigned int *hist, SelState *st, int n_depth, int pass) {
-    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (d >= n_depth) return;
     SelState s = st[d];
-    if (s.k == 0) return;   // done in an earlier pass
+    if (s.k == 0) return;   // done in an earlier pass (warp-uniform)
     const int shift = 56 - 8 * pass;
+    unsigned int h[8];
+    unsigned long long tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) { h[q] = hist[d * 256 + 255 - 8 * lane - q]; tot += h[q]; }
+    unsigned long long incl = tot;   // inclusive scan over lanes (descending digits)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const unsigned reach = __ballot_sync(0xffffffffu, incl >= s.k);
+    const int src = __ffs(reach) - 1;          // first lane whose prefix reaches k (k <= the total: exists)
     unsigned long long cum = 0, cnt = 0;
     int digit = 0;
-    for (int b = 255; b >= 0; b--) {
-        const unsigned long long c = hist[d * 256 + b];
-        if (cum + c >= s.k) { digit = b; cnt = c; break; }
-        cum += c;
+    if (lane == src) {
+        cum = incl - tot;                      // keys in the digits above this lane's
+        for (int q = 0; q < 8; q++) {
+            if (cum + h[q] >= s.k) { digit = 255 - 8 * lane - q; cnt = h[q]; break; }
+            cum += h[q];
+        }
     }
+#pragma unroll
+    for (int q = 0; q < 8; q++) hist[d * 256 + 255 - 8 * lane - q] = 0;
+    if (lane != src) return;
     s.k -= cum;
     s.prefix |= (unsigned long long)digit << shift;
     s.mask |= 0xFFull << shift;
@@ -169,7 +189,6 @@ __global__ void select_pick_kernel(unsigned int *hist, SelState *st, int n_depth
     // top-N_r set, so the remaining passes skip this depth (k = 0 marks it)
     if (cnt == s.k) s.k = 0;
     st[d] = s;
-    for (int b = 0; b < 256; b++) hist[d * 256 + b] = 0;
 }
 
 __global__ void select_init_kernel(const void *tables, SelState *st, int n_depth) {
@@ -365,7 +384,7 @@ cudaError_t launch_select(const TableHeader &h, const void *d_tables, const uint
         count_launches(1);
         select_hist_kernel<<<(unsigned)h.total_ctas, 256, 0, s>>>(d_tables, coef_key, hist, st, n_depth, pass);
         count_launches(1);
-        select_pick_kernel<<<(n_depth + 127) / 128, 128, 0, s>>>(hist, st, n_depth, pass);
+        select_pick_kernel<<<(n_depth * 32 + 127) / 128, 128, 0, s>>>(hist, st, n_depth, pass);   // a warp per depth
     }
     return cudaGetLastError();
 }
