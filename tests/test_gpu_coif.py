@@ -128,6 +128,21 @@ def test_coif_fused_tiles_equal_line_passes(W, name, row0, row1, kw):
     assert float(u_f.abs().max()) > 0
 
 
+def test_coif_hologram_host_print_only_uses_fused_tiles(W):
+    """wasabi_hologram_host without u (print only) takes the fused tile synthesis; its bits equal the
+    device path's (which writes u to its own buffer) bit for bit."""
+    import torch
+    cfg = CONFIGS["C2"].replace(levels=3)
+    pts = make_points(cfg, n=2000)
+    p = gpu_params(cfg, wavelet=1)
+    pl, _, u_g, bits_g = _gpu_run(W, cfg, pts, 512, 1024, wavelet=1)
+    ws = torch.empty(W.hologram_workspace_bytes(p, len(pts), 512, 1024), dtype=torch.uint8, device="cuda")
+    h_bits = torch.empty((512, p.n_h // 8), dtype=torch.uint8)
+    W.hologram_host(p, W.PrintParams(), torch.from_numpy(pts), 512, 1024, ws, h_bits)
+    torch.cuda.synchronize()
+    assert np.array_equal(h_bits.numpy(), bits_g)
+
+
 def test_coif_fused_entry_refuses(W):
     import torch
     cfg = CONFIGS["C1"]
