@@ -404,6 +404,10 @@ def run_ours(args, cfg):
                               "peak_source": "148 SMs x f_SM x 8 acc/clk (shared-memory RMW, conflict-free)"}
     if onchip:
         roofline["onchip"] = onchip
+    # every timed stage against the HBM peak (algorithmic bytes of the stage / its event time)
+    roofline["stages"] = {k: {"alg_bytes": alg[k], "achieved": alg[k] / (stage_ms[k] * 1e-3) / 1e9,
+                              "frac": alg[k] / (stage_ms[k] * 1e-3) / 1e9 / hbm[0]}
+                          for k in stage_ms if k in alg and stage_ms[k] > 0}
 
     # the other band partition, timed the same way (N > 1 only)
     alt = None
