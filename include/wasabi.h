@@ -269,6 +269,8 @@ wasabi_status wasabi_hologram_workspace_bytes(const wasabi_params *params, int64
 /* Whole hot path from HOST buffers: H2D copy of h_points (n x 4 float32), steps 1-4 for band
  * [row0, row1) (steps 2b-4 through wasabi_superpose_inverse), D2H copy of the bits (h_bits, (row1-row0) x n_h/8 bytes) and, if h_u != NULL,
  * of u ((row1-row0) x n_h complex64).  Host buffers should be pinned for asynchronous copies.
+ * WASABI_FLAG_COIFLET: psi on the halo band (wasabi_superpose), then wasabi_inverse_wt -- fused tiles
+ * when h_u == NULL (print only), the in-place line passes when u is wanted (u = the band rows of psi).
  * Returns after enqueueing; the caller synchronises `stream` before reading h_bits / h_u. */
 wasabi_status wasabi_hologram_host(const wasabi_params *params, const wasabi_print_params *print,
                                    const float *h_points, int64_t n, int64_t row0, int64_t row1,
