@@ -334,6 +334,25 @@ def run_ours(args, cfg):
     bands = parts[mode]
     row0, row1 = bands[rank]
     pl, own_ms, stage_ms, launches, ck = timed_run(bands, args.steps, args.warmup, True)
+    graph = None
+    if world == 1 and not args.unfused and cfg.n_h < 65536:
+        # the same step as one CUDA graph (Pipeline.capture / replay): what the launch overhead costs
+        # the small configs; reported beside the eager line, not instead of it
+        pl.capture(d_pts)
+        for _ in range(args.warmup):
+            pl.replay()
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        torch.cuda.synchronize(dev)
+        for e0, e1 in gev:
+            if flush is not None:
+                flush.zero_()
+            e0.record(stream)
+            pl.replay()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        g_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in gev)
+        graph = {"ms_per_step": g_ms, "value": cfg.n_h * cfg.n_h / (g_ms * 1e-3) / 1e9, "unit": "Gpixel/s",
+                 "note": "one CUDA graph per step (tables + bins + fused kernel), L2 flushed between replays"}
     t_ms = max_over_ranks(own_ms)
     stage_ms = {s: max_over_ranks(v) for s, v in stage_ms.items()}
     ms_per_step = t_ms / args.steps
@@ -473,7 +492,7 @@ def run_ours(args, cfg):
                "points_per_s": points_per_s, "stage_ms": stage_ms, "bin_entries": st["entries"],
                "accumulations": sum(r["acc"] for r in per_rank),
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-               "clocks": ck, "per_rank": per_rank, "bands_alt": alt, "assembled": assembled,
+               "clocks": ck, "graph": graph, "per_rank": per_rank, "bands_alt": alt, "assembled": assembled,
                "checksum": {"bits_set": cs[3]},
                "paper_context": {"wasabi_s_65536sq_95949pts_cpu": 354, "nlut_s": 10533,
                                  "cite": "PAPER.md:166 (Xeon E5 v3; different point count and wavelet)"}}
