@@ -276,6 +276,11 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
         return tile[(swz(tile_sa + 8u * (uint32_t)(M + r * S + x)) - tile_sa) >> 3];
     };
 
+    // the tile's bin pointers first: their load chain (bin -> point -> descriptor -> window pointers ->
+    // first chunks) overlaps the zero fill, whose completion is awaited only before the first
+    // shared-memory access of the ring
+    const unsigned long long b1 = bptr[t + 1];
+    unsigned long long pb = bptr[t];
 #if WASABI_BULKZERO
     // zero the tile + dummy block by one bulk async copy from a zero buffer (the copy engine, not the
     // LSU); the mbarrier sits after the dummy block
@@ -291,9 +296,7 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                          ::"r"(tile_sa), "l"(g_zero), "r"(zbytes), "r"(mbar) : "memory");
         }
-        __syncthreads();
-        asm volatile("{\n .reg .pred p;\n WZ_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-                     " @!p bra WZ_%=;\n}" ::"r"(mbar) : "memory");
+        __syncthreads();   // the mbarrier is initialised; the wait is deferred to just before the ring
     }
 #else
     for (int i = threadIdx.x; i < kData + 8; i += NT) tile[i] = make_float2(0.f, 0.f);
@@ -302,8 +305,6 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
 
     const int lv0 = superpose_class_level(cls, 0, A.L), lv1 = superpose_class_level(cls, 1, A.L);
     const int lv2 = superpose_class_level(cls, 2, A.L);
-    const unsigned long long b1 = bptr[t + 1];
-    unsigned long long pb = bptr[t];
 
     // batch state: lane = point; per level slot j its range: first entry beg and pk = (smem base << 16)
     // | length; the CURRENT batch (beg, pk, a_l) and the NEXT one (nbeg, npk, na), loaded while the
@@ -453,9 +454,19 @@ __global__ void __launch_bounds__(2 * T, T == 64 ? WASABI_MINB : 1) superpose_ke
     // body with the chunks of the new batch in flight, fetches the batch after it (the window-pointer
     // loads overlap those chunks) and re-enters without draining.  The batch code stays inlined once
     // (fetch, outside the ring body).  The ring drains only at the tile's last batch.
-    if (have) {
+    const int had = have;   // the prefetches may exhaust a small tile (have = 0): its chunks still get consumed
+    if (had) {
 #pragma unroll
         for (int u = 0; u < kD; u++) WASABI_PREFETCH(u);
+    }
+#if WASABI_BULKZERO
+    {
+        const uint32_t mbar = tile_sa + 8u * (uint32_t)(kData + 8);
+        asm volatile("{\n .reg .pred p;\n WZ_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+                     " @!p bra WZ_%=;\n}" ::"r"(mbar) : "memory");
+    }
+#endif
+    if (had) {
         while (true) {
             bool more = true;
             while (more) {
